@@ -1,0 +1,468 @@
+#!/usr/bin/env python
+"""Benchmark of the colored DG surface-integral hot path (driver contract).
+
+One "step" = one SSP-RK3 time step of 2D Euler DG p=2 with the
+Lax-Friedrichs flux on config c2 (``shuffle_elements(gen_tri_rect(708, 708),
+0)``: 1,002,528 triangles, 1,505,208 edges, 3 colors, fp64), i.e. three
+fused colored RHS evaluations (BASELINE.json configs[1]).  Inputs are
+synthetic (a smooth density wave on the far-field stream) and device
+resident (0.19 GB per state array, larger than the 126 MB L2).
+
+value  = surface-integral edge evaluations per second = 3 * n_surfaces / t_step
+e2e    = the same through the public host-buffer API (mc_dg_ssprk3_host:
+         H2D of the state, the step, D2H of the state)
+roofline = the colored surface kernel (k_surface_colored): algorithmic bytes
+         per launch / its CUDA-event duration, against
+         the measured HBM copy peak in MEASURED_PEAKS.json
+cpu_baseline / --impl reference = the numpy fp64 oracle (oracle/dg_oracle.py,
+         a port: the reference has no DG) on a bounded sample of the same
+         workload.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                       [--config c1|c2|c3|c4|c5] [--variants] [--no-cpu]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "surface-integral edges/sec & DOF-updates/sec; % of HBM roofline; 1/2/4/8 GPU"
+UNIT = "edges/s"
+
+
+# ------------------------------------------------------------- workloads
+def config_spec(name: str):
+    import paper_1601_07613_b200 as P
+    if name == "c1":
+        return dict(desc="2D scalar advection DG p=1, gen_tri_rect(64,64), 3 colors",
+                    build=lambda: P.gen_tri_rect(64, 64), physics="advection", p=1,
+                    sample=lambda: P.gen_tri_rect(64, 64))
+    if name == "c2":
+        return dict(desc="2D Euler DG p=2, shuffle_elements(gen_tri_rect(708,708),0), LF, 3 colors",
+                    build=lambda: P.shuffle_elements(P.gen_tri_rect(708, 708), 0),
+                    physics="euler", p=2,
+                    sample=lambda: P.shuffle_elements(P.gen_tri_rect(177, 177), 0))
+    if name == "c3":
+        return dict(desc="2D Euler DG p=3, gen_quad_rect(2000,2000), LF, 4 colors",
+                    build=lambda: P.gen_quad_rect(2000, 2000), physics="euler", p=3,
+                    sample=lambda: P.gen_quad_rect(250, 250))
+    if name == "c4":
+        return dict(desc="3D Euler DG p=2, gen_tet_prism(110,110,110), LF, 4 colors",
+                    build=lambda: P.gen_tet_prism(110, 110, 110), physics="euler", p=2,
+                    sample=lambda: P.gen_tet_prism(28, 28, 28))
+    if name == "c5":
+        def build():
+            base = P.gen_tri_rect(708, 708)
+            col, _ = P.color(base)
+            cen = base.vertices[base.elem_verts[:, :3]].mean(axis=1)
+            tg = np.flatnonzero(((cen - 354.0) ** 2).sum(1) <= 177.0 ** 2)
+            return P.refine(base, col, tg)
+
+        def sample():
+            base = P.gen_tri_rect(177, 177)
+            col, _ = P.color(base)
+            cen = base.vertices[base.elem_verts[:, :3]].mean(axis=1)
+            tg = np.flatnonzero(((cen - 88.5) ** 2).sum(1) <= 44.25 ** 2)
+            return P.refine(base, col, tg)
+        return dict(desc="2D Euler DG p=2, 1:4 refined disc r=177 in gen_tri_rect(708,708), "
+                         "6 colors, mortars", build=build, physics="euler", p=2,
+                    sample=sample)
+    raise SystemExit(f"unknown config {name}")
+
+
+def build_operator(spec, which="build"):
+    from paper_1601_07613_b200.dg import DGOperator
+    import paper_1601_07613_b200 as P
+    obj = spec[which]()
+    if isinstance(obj, tuple):          # (RefinedMesh, 6-coloring)
+        return DGOperator(obj[0], obj[1], degree=spec["p"], physics=spec["physics"])
+    col, _ = P.color(obj)
+    return DGOperator(obj, col, degree=spec["p"], physics=spec["physics"])
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML clock / throttle-reason sampling during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int = 0, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nvml:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nvml:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# -------------------------------------------------------------- roofline
+def launch_bytes(op, color: int, rk_mode: int, a: float) -> int:
+    """Algorithmic bytes of one colored launch:
+    per surface the metadata (ids, code word, geometry), per present side
+    its U block, the inverse Jacobian at first touch, the residual block
+    read unless first touch, and either the residual write or, at the last
+    touch of an RK stage, the U0 read (a != 0) / U0 save / U write."""
+    sl = op.surfaces
+    b0, b1 = sl.bounds[color - 1], sl.bounds[color]
+    code = sl.code[b0:b1].astype(np.int64)
+    right = sl.right[b0:b1]
+    D = op.n_equations * op.n_basis * 8
+    dim = op.dim
+    meta = 4 + 4 + 4 + 8 * (dim + 2)
+    total = meta * (b1 - b0)
+    for side, fbit, lbit in ((0, 1 << 12, 1 << 13), (1, 1 << 14, 1 << 15)):
+        present = np.ones(b1 - b0, bool) if side == 0 else right >= 0
+        ghost = np.zeros(b1 - b0, bool) if side == 0 else (code & (1 << 16)) != 0
+        first = present & ~ghost & ((code & fbit) != 0)
+        last = present & ~ghost & ((code & lbit) != 0)
+        owner = present & ~ghost
+        total += D * int(present.sum())                       # U read
+        total += 8 * dim * dim * int(first.sum())             # Jinv at first touch
+        total += D * int((owner & ~first).sum())              # R read
+        if rk_mode == 0:
+            total += D * int(owner.sum())                     # R write
+        else:
+            total += D * int((owner & ~last).sum())           # R write
+            total += D * int(last.sum())                      # U write
+            if a != 0.0:
+                total += D * int(last.sum())                  # U0 read
+            if rk_mode == 2:
+                total += D * int(last.sum())                  # U0 save
+    return int(total)
+
+
+STAGES = ((2, 0.0, 1.0), (1, 0.75, 0.25), (1, 1.0 / 3.0, 2.0 / 3.0))
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- CPU leg
+def cpu_sample(spec, steps=1):
+    """Oracle (numpy fp64) SSP-RK3 on the bounded sample; edges/s."""
+    import paper_1601_07613_b200 as P
+    from oracle import dg_oracle as D
+    from paper_1601_07613_b200.dg.operator import default_freestream
+    obj = spec["sample"]()
+    if isinstance(obj, tuple):
+        ref, fine = obj
+        mesh, col, mortars = ref.mesh, fine, ref.hanging_array()
+    else:
+        mesh = obj
+        col, _ = P.color(mesh)
+        mortars = None
+    dim = mesh.dim
+    phys = D.Physics(spec["physics"], dim,
+                     farfield=(0.0,) if spec["physics"] == "advection" else default_freestream(dim))
+    se = mesh.surf_elems.copy()
+    active = np.ones(mesh.n_surfaces, bool)
+    if mortars is not None and len(mortars):
+        for k in (1, 2):
+            se[mortars[:, k], 1] = se[mortars[:, 0], 0]
+        active[mortars[:, 0]] = False
+    kind = {"tri": "tri", "quad": "quad", "tet": "tet"}[next(iter(mesh.element_kind_profile)).value]
+    prob = D.Problem(kind, spec["p"], phys, mesh.vertices, mesh.elem_verts, mesh.surf_verts, se,
+                     col.colors, col.n_colors, active)
+    D.setup(prob)
+    neq = phys.neq
+    nb = D.Basis(kind, spec["p"]).scale.size
+    U = np.zeros((mesh.n_elements, neq, nb))
+    ff = np.asarray(phys.farfield) if spec["physics"] == "euler" else np.ones(1)
+    U[:, :, 0] = ff[None, :] * (1.0 / D.Basis(kind, spec["p"]).scale[0])
+    t0 = time.perf_counter()
+    D.ssprk3(prob, U, 1e-3, steps)
+    dt = time.perf_counter() - t0
+    ns = int(active.sum())
+    return 3 * steps * ns / dt, dt, mesh.n_elements, ns
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port on the same config (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    spec = config_spec(args.config)
+    import paper_1601_07613_b200 as P  # noqa: F401  (mesh setup helpers only)
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        cpu_sample(spec, 1)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, t, ne, ns = cpu_sample(spec, 1)
+        rates.append(r)
+        times.append(t)
+    value = float(np.median(rates))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * float(np.median(times)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": spec["desc"], "sample_elements": ne, "sample_surfaces": ns},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"oracle/dg_oracle.py SSP-RK3 step on a {ne}-element, "
+                                   f"{ns}-surface mesh of the same family"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--variants", action="store_true",
+                    help="also time buffered/atomic strategies and the integer sweeps")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    spec = config_spec(args.config)
+    t_setup = time.perf_counter()
+    op = build_operator(spec)
+    t_setup = time.perf_counter() - t_setup
+    U_host = op.initial_state("wave")
+    dt = op.stable_dt(0.2)
+    U = op.to_device(U_host)
+    work = op.work_device()
+    U0, R = work[0], work[1]
+    stream = torch.cuda.current_stream()
+    nc = op.n_colors
+
+    def step(events=None):
+        for mode, a, b in STAGES:
+            for c in range(1, nc + 1):
+                if events is not None:
+                    ev = torch.cuda.Event(enable_timing=True)
+                    ev.record(stream)
+                    events.append((mode, a, c, ev))
+                op.color_pass_device(c, U, U0, R, mode, a, b, dt, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    barrier()
+    events = []
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            step(events)
+        end.record(stream)
+        end.synchronize()
+    barrier()
+    total_ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / max(args.steps, 1)
+    ns, ne = op.n_surfaces, op.n_elements
+    value = world * 3 * ns / (ms_per_step * 1e-3)
+    dof_rate = world * ne * op.n_basis * op.n_equations * 3 / (ms_per_step * 1e-3)
+
+    # per-launch durations of k_surface_colored from the timed region
+    per = {}
+    marks = events + [(None, None, None, end)]
+    for (mode, a, c, ev), (_, _, _, nxt) in zip(events, marks[1:]):
+        per.setdefault((mode, a, c), []).append(ev.elapsed_time(nxt))
+    bytes_step, ms_step = 0, 0.0
+    by_color = {}
+    for (mode, a, c), ts in per.items():
+        avg = float(np.mean(ts))
+        by = launch_bytes(op, c, mode, a)
+        bytes_step += by
+        ms_step += avg
+        by_color.setdefault(c, [0, 0.0])
+        by_color[c][0] += by
+        by_color[c][1] += avg
+    peak, peak_src = peaks()
+    achieved = bytes_step / (ms_step * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{args.config}.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch_avg")
+        except Exception:
+            traffic = None
+
+    # correctness guard: the state must stay finite
+    finite = bool(torch.isfinite(U).all().item())
+
+    # end-to-end through the public host-buffer API
+    pinned = torch.empty((ne, op.stride), dtype=torch.float64, pin_memory=True)
+    host = pinned.numpy()
+    host[:] = op.to_internal(U_host)
+    op.ssprk3_host_internal(host, dt, 1)          # warm (allocates scratch)
+    host[:] = op.to_internal(U_host)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        op.ssprk3_host_internal(host, dt, 1)
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    e2e_value = world * 3 * ns / e2e_s
+    state_bytes = ne * op.stride * 8
+
+    comparisons = None
+    if args.variants:
+        comparisons = variants(op, U_host, spec, stream)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        r, t, sne, sns = cpu_sample(spec, 1)
+        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"oracle/dg_oracle.py numpy fp64 SSP-RK3 step, {sne} elements / "
+                         f"{sns} surfaces of the same mesh family ({t:.1f} s)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (density wave on far-field stream)",
+        "config": {"workload": spec["desc"], "elements": ne, "surfaces": ns, "colors": nc,
+                   "degree": op.degree, "n_basis": op.n_basis, "n_equations": op.n_equations,
+                   "step": "1 SSP-RK3 step = 3 fused colored RHS (volume fused into first "
+                           "color pass, RK update into last)",
+                   "l2": f"inputs larger than L2 (state {state_bytes / 1e9:.2f} GB x 3 arrays)",
+                   "parallelism": "single-GPU" if world == 1 else f"replicas x{world}",
+                   "setup_s": round(t_setup, 2)},
+        "dof_updates_per_s": dof_rate,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac_of_8tbs_nominal": achieved / 8000.0,
+                     "kernel": "k_surface_colored",
+                     "algorithmic_bytes_per_step": bytes_step,
+                     "kernel_ms_per_step": ms_step,
+                     "per_color_gbs": {str(c): v[0] / (v[1] * 1e-3) / 1e9
+                                       for c, v in sorted(by_color.items())}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+                "d2h_bytes_per_step": state_bytes},
+        "gpu_launches": args.steps * 3 * nc,
+        "clocks": clk.summary(),
+        "finite": finite,
+    }
+    if comparisons is not None:
+        line["comparisons"] = comparisons
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def variants(op, U_host, spec, stream, reps=5):
+    """The paper's comparisons on the same mesh: colored vs buffered vs
+    atomic RHS, buffer memory avoided, and the integer-payload sweeps."""
+    import torch
+    import paper_1601_07613_b200 as P
+    from paper_1601_07613_b200.sweeps import DeviceLayout
+    out = {}
+    U = op.to_device(U_host)
+    R = torch.zeros_like(U)
+
+    def timeit(fn):
+        fn()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    for strat in ("colored", "buffered", "atomic"):
+        ms = timeit(lambda: op.rhs_device(U, R, strat, stream))
+        out[f"rhs_{strat}_ms"] = ms
+        out[f"rhs_{strat}_edges_per_s"] = op.n_surfaces / (ms * 1e-3)
+    mem = P.memory_saved(op.degree, op.n_equations, op.n_surfaces,
+                         {"tri": "tri", "quad": "quad", "tet": "tet"}[op.kind.value])
+    out["buffer_bytes_avoided"] = mem.n_bytes
+    out["buffer_gb_truncated"] = mem.gb_truncated
+    # integer Algorithm 1 on the reordered mesh
+    lay = DeviceLayout(op.layout_mesh, op.layout_coloring)
+    pay = torch.from_numpy(P.default_payload(op.n_surfaces)).cuda()
+    tot = torch.zeros(op.n_elements, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(2 * op.n_surfaces, dtype=torch.int64, device="cuda")
+    for name, fn in (("int_colored", lambda: lay.sweep_colored(pay, tot, stream)),
+                     ("int_buffered", lambda: lay.sweep_buffered(pay, buf, tot, stream)),
+                     ("int_atomic", lambda: lay.sweep_atomic(pay, tot, stream))):
+        ms = timeit(fn)
+        out[f"{name}_ms"] = ms
+        out[f"{name}_edges_per_s"] = op.n_surfaces / (ms * 1e-3)
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -166,9 +166,9 @@ typedef struct mc_dg_desc {
   const uint32_t* surf_code;       /* ns, side codes + flags            */
   const double* surf_geom;         /* ns x (dim+2): n_0..n_{d-1}, sL, sR */
   const double* elem_jinv;         /* (ne+ng) x dim x dim, dxi_r/dx_d   */
-  const int32_t* elem_surfs;       /* ne x 4 surface slots (-1 pad), for
-                                      the buffered gather; slot = list id */
-  const int8_t* elem_side_of;      /* ne x 4: 0 = left, 1 = right        */
+  const int64_t* elem_slot_ptr;    /* ne+1 CSR offsets (buffered gather) */
+  const int32_t* elem_slots;       /* buffer slots 2*s+side per element,
+                                      local side order                    */
   /* reference-element tables (host), see dg/tables.py */
   int n_face_codes, n_face_q, n_vol_q, n_basis;
   const double* face_phi;  /* n_face_codes x n_face_q x n_basis */
@@ -201,6 +201,13 @@ int mc_dg_rhs(mc_dg* dg, const double* U_dev, double* R_dev, int strategy,
 int mc_dg_rk_stage(mc_dg* dg, double* U_dev, const double* U0_dev,
                    double* R_scratch_dev, double a, double b, double dt,
                    void* stream);
+/* One color launch of the colored strategy (what mc_dg_rhs / rk_stage /
+ * ssprk3 issue n_colors times); rk_mode 0 = residual only, 1 = RK stage
+ * update in last-touch sides, 2 = as 1 and save U0 := U first.  Exposed so
+ * callers can time or interleave individual color launches. */
+int mc_dg_color_pass(mc_dg* dg, int color, double* U_dev, double* U0_dev,
+                     double* R_dev, int rk_mode, double a, double b, double dt,
+                     void* stream);
 /* n_steps SSP-RK3 steps; work_dev = 2 blocks arrays (U0, R scratch). */
 int mc_dg_ssprk3(mc_dg* dg, double* U_dev, double* work_dev, double dt,
                  int n_steps, void* stream);

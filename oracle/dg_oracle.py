@@ -1,0 +1,420 @@
+"""DG right-hand side of Eq. (2) restated in numpy fp64 (oracle; test
+infrastructure).
+
+PARITY UNPINNED BY THE REFERENCE: the reference puts the DG discretisation
+out of scope (sweeps.py:1-24) — there is no reference
+flux, basis or quadrature to compare with.  This oracle follows the paper's
+Eq. (2) and Algorithm 1's accumulation order
+ and is anchored by independent known-answer tests
+(tests/test_dg_oracle.py): orthonormality, free-stream preservation,
+conservation (closed mesh -> zero mass residual; open mesh -> boundary
+flux), and p+1 convergence for linear advection.
+
+It is written independently of the product (paper_1601_07613_b200.dg):
+* basis: Dubiner/Legendre modes through collapsed coordinates, own Jacobi
+  recurrence, gradients by complex-step differentiation;
+* quadrature: own Golub-Welsch Gauss-Jacobi;
+* trace points: mapped from PHYSICAL surface points back into each
+  element by the inverse affine map (no side-code tables), so orientation
+  and mortar sub-interval handling are checked, not shared.
+
+Discretisation: U_e = sum_j c_ej phi_j(xi), phi orthonormal
+on the reference element, affine elements, so
+  dc_ej/dt = sum_q w_q grad_xi phi_j(q) . (Jinv F(U_e(q)))
+             -/+ (|S| / |det J_e|) sum_g w_g phi_j(xi_e(x_g)) Fhat_g . n
+with n the unit normal out of the LEFT element, '-' for the left element,
+'+' for the right; Fhat is local Lax-Friedrichs (Rusanov), which for linear
+advection is upwind; physical boundaries see a constant far-field state.
+Per element the order of accumulation is: volume, then color 1, 2, ...
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+SIDES = {"tri": ((0, 1), (1, 2), (2, 0)), "quad": ((0, 1), (1, 2), (2, 3), (3, 0)),
+         "tet": ((0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3))}
+NVERT = {"tri": 3, "quad": 4, "tet": 4}
+DIMS = {"tri": 2, "quad": 2, "tet": 3}
+
+
+# ----------------------------------------------------------- quadrature
+def gauss_jacobi(n: int, alpha: float, beta: float = 0.0):
+    """Golub-Welsch nodes/weights on [-1, 1] for (1-x)^a (1+x)^b."""
+    from math import gamma
+    k = np.arange(n, dtype=np.float64)
+    ab = alpha + beta
+    diag = np.empty(n)
+    for i in range(n):
+        d = (2 * i + ab) * (2 * i + ab + 2)
+        diag[i] = (beta - alpha) / (ab + 2) if (i == 0 and ab == 0) else \
+            (beta ** 2 - alpha ** 2) / d if d != 0 else (beta - alpha) / (ab + 2)
+    off = np.empty(max(n - 1, 0))
+    for i in range(1, n):
+        num = 4 * i * (i + alpha) * (i + beta) * (i + ab)
+        den = (2 * i + ab) ** 2 * (2 * i + ab + 1) * (2 * i + ab - 1)
+        off[i - 1] = np.sqrt(num / den)
+    T = np.diag(diag) + np.diag(off, 1) + np.diag(off, -1)
+    x, V = np.linalg.eigh(T)
+    mu0 = 2 ** (ab + 1) * gamma(alpha + 1) * gamma(beta + 1) / gamma(ab + 2)
+    return x, mu0 * V[0] ** 2
+
+
+def vol_rule(kind: str, p: int):
+    n = p + 1
+    a, wa = gauss_jacobi(n, 0.0)
+    if kind == "quad":
+        t = 0.5 * (a + 1)
+        wt = 0.5 * wa
+        P = np.array([[x, y] for x in t for y in t])
+        W = np.array([u * v for u in wt for v in wt])
+        return P, W
+    b, wb = gauss_jacobi(n, 1.0)
+    if kind == "tri":
+        P, W = [], []
+        for x, u in zip(a, wa):
+            for y, v in zip(b, wb):
+                P.append([(1 + x) * (1 - y) / 4, (1 + y) / 2])
+                W.append(u * v / 8)
+        return np.array(P), np.array(W)
+    c, wc = gauss_jacobi(n, 2.0)
+    P, W = [], []
+    for x, u in zip(a, wa):
+        for y, v in zip(b, wb):
+            for z, w in zip(c, wc):
+                P.append([(1 + x) * (1 - y) * (1 - z) / 8, (1 + y) * (1 - z) / 4, (1 + z) / 2])
+                W.append(u * v * w / 64)
+    return np.array(P), np.array(W)
+
+
+def surf_rule(kind: str, p: int):
+    """Points in surface parameters (edge t, or face barycentrics), weights sum 1."""
+    if kind != "tet":
+        a, wa = gauss_jacobi(p + 1, 0.0)
+        return 0.5 * (a + 1)[:, None], 0.5 * wa
+    P, W = vol_rule("tri", p)
+    return np.stack([1 - P[:, 0] - P[:, 1], P[:, 0], P[:, 1]], axis=1), 2 * W
+
+
+# ------------------------------------------------------------------ basis
+def jacobi(n, alpha, x):
+    """P_n^(alpha,0)(x) by recurrence (works on complex arrays)."""
+    beta = 0.0
+    p0 = np.ones_like(x)
+    if n == 0:
+        return p0
+    p1 = 0.5 * ((alpha + beta + 2) * x + (alpha - beta))
+    for m in range(2, n + 1):
+        s = 2 * m + alpha + beta
+        p2 = ((s - 1) * ((s * (s - 2)) * x + alpha ** 2 - beta ** 2) * p1
+              - 2 * (m + alpha - 1) * (m + beta - 1) * s * p0) / (2 * m * (m + alpha + beta) * (s - 2))
+        p0, p1 = p1, p2
+    return p1
+
+
+def mode_list(kind, p):
+    if kind == "quad":
+        return [(i, j) for i in range(p + 1) for j in range(p + 1)]
+    if kind == "tri":
+        return [(n - j, j) for n in range(p + 1) for j in range(n + 1)]
+    return [(i, j, n - i - j) for n in range(p + 1) for i in range(n, -1, -1)
+            for j in range(n - i, -1, -1)]
+
+
+def _safe_div(num, den):
+    den = np.where(den == 0, 1.0, den)
+    return num / den
+
+
+def raw_mode(kind, mode, X):
+    """Unnormalised mode at reference points X (npts, dim), complex ok."""
+    if kind == "quad":
+        i, j = mode
+        return jacobi(i, 0.0, 2 * X[:, 0] - 1) * jacobi(j, 0.0, 2 * X[:, 1] - 1)
+    if kind == "tri":
+        i, j = mode
+        xi, eta = X[:, 0], X[:, 1]
+        a = _safe_div(2 * xi, 1 - eta) - 1
+        return jacobi(i, 0.0, a) * (1 - eta) ** i * jacobi(j, 2 * i + 1.0, 2 * eta - 1)
+    i, j, k = mode
+    xi, eta, zeta = X[:, 0], X[:, 1], X[:, 2]
+    a = _safe_div(2 * xi, 1 - eta - zeta) - 1
+    b = _safe_div(2 * eta, 1 - zeta) - 1
+    return (jacobi(i, 0.0, a) * (1 - eta - zeta) ** i * jacobi(j, 2 * i + 1.0, b)
+            * (1 - zeta) ** j * jacobi(k, 2 * i + 2 * j + 2.0, 2 * zeta - 1))
+
+
+class Basis:
+    def __init__(self, kind, p):
+        self.kind, self.p = kind, p
+        self.modes = mode_list(kind, p)
+        P, W = vol_rule(kind, p + 1)
+        self.scale = np.array([1 / np.sqrt(np.sum(W * raw_mode(kind, m, P).real ** 2))
+                               for m in self.modes])
+
+    def values(self, X):
+        return np.stack([raw_mode(self.kind, m, X).real * s
+                         for m, s in zip(self.modes, self.scale)], axis=-1)
+
+    def gradients(self, X):
+        """(dim, npts, nb) by complex-step differentiation."""
+        h = 1e-30
+        out = []
+        for r in range(X.shape[1]):
+            Xc = X.astype(np.complex128)
+            Xc[:, r] += 1j * h
+            out.append(np.stack([raw_mode(self.kind, m, Xc).imag / h * s
+                                 for m, s in zip(self.modes, self.scale)], axis=-1))
+        return np.stack(out)
+
+
+# ---------------------------------------------------------------- physics
+@dataclass
+class Physics:
+    name: str                   # "advection" | "euler"
+    dim: int
+    gamma: float = 1.4
+    velocity: tuple = (1.0, 0.5, 0.25)
+    farfield: tuple = (0.0,)
+
+    @property
+    def neq(self):
+        return 1 if self.name == "advection" else self.dim + 2
+
+    def flux(self, U):
+        """U (..., neq) -> F (..., dim, neq)."""
+        if self.name == "advection":
+            a = np.asarray(self.velocity[: self.dim])
+            return U[..., None, :] * a[:, None]
+        rho = U[..., 0]
+        mom = U[..., 1:1 + self.dim]
+        E = U[..., -1]
+        vel = mom / rho[..., None]
+        pres = (self.gamma - 1) * (E - 0.5 * (mom * vel).sum(-1))
+        F = np.zeros(U.shape[:-1] + (self.dim, self.neq))
+        for d in range(self.dim):
+            F[..., d, 0] = mom[..., d]
+            F[..., d, 1:1 + self.dim] = mom[..., d, None] * vel
+            F[..., d, 1 + d] += pres
+            F[..., d, -1] = (E + pres) * vel[..., d]
+        return F
+
+    def wave_speed(self, U, n):
+        if self.name == "advection":
+            return np.abs((np.asarray(self.velocity[: self.dim]) * n).sum(-1))
+        rho = U[..., 0]
+        vel = U[..., 1:1 + self.dim] / rho[..., None]
+        E = U[..., -1]
+        pres = (self.gamma - 1) * (E - 0.5 * rho * (vel * vel).sum(-1))
+        return np.abs((vel * n).sum(-1)) + np.sqrt(self.gamma * pres / rho)
+
+    def numerical_flux(self, UL, UR, n):
+        """Local Lax-Friedrichs; n broadcast over quadrature points."""
+        FL = (self.flux(UL) * n[..., :, None]).sum(-2)
+        FR = (self.flux(UR) * n[..., :, None]).sum(-2)
+        lam = np.maximum(self.wave_speed(UL, n), self.wave_speed(UR, n))
+        return 0.5 * (FL + FR) - 0.5 * lam[..., None] * (UR - UL)
+
+
+# ----------------------------------------------------------------- problem
+@dataclass
+class Problem:
+    kind: str
+    p: int
+    physics: Physics
+    vertices: np.ndarray
+    elem_verts: np.ndarray
+    surf_verts: np.ndarray
+    surf_elems: np.ndarray      # (ns, 2); mortar halves carry the coarse right
+    colors: np.ndarray
+    n_colors: int
+    active: np.ndarray          # surfaces taking part (full coarse edges off)
+    period: tuple | None = None
+    cache: dict = field(default_factory=dict)
+
+
+def element_coords(prob: Problem):
+    X = prob.vertices[prob.elem_verts[:, :NVERT[prob.kind]]].copy()
+    if prob.period is not None:
+        for d, L in enumerate(prob.period):
+            if L:
+                X[:, :, d] -= L * np.round((X[:, :, d] - X[:, :1, d]) / L)
+    return X
+
+
+def _affine(kind, X):
+    if kind == "quad":
+        J = np.stack([X[:, 1] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)
+    else:
+        J = np.stack([X[:, r + 1] - X[:, 0] for r in range(DIMS[kind])], axis=2)
+    return J, np.linalg.det(J), np.linalg.inv(J)
+
+
+def _to_ref(Jinv, x0, x, period, centre):
+    """Reference coordinates of physical points x (n, g, d) in elements."""
+    x = x.copy()
+    if period is not None:
+        for d, L in enumerate(period):
+            if L:
+                x[..., d] -= L * np.round((x[..., d] - centre[:, None, d]) / L)
+    return np.einsum("nrd,ngd->ngr", Jinv, x - x0[:, None, :])
+
+
+def setup(prob: Problem):
+    c = prob.cache
+    if c:
+        return c
+    kind, p = prob.kind, prob.p
+    B = Basis(kind, p)
+    X = element_coords(prob)
+    J, det, Jinv = _affine(kind, X)
+    vP, vW = vol_rule(kind, p)
+    fP, fW = surf_rule(kind, p)
+    c.update(B=B, X=X, det=det, Jinv=Jinv, vW=vW, fW=fW, vphi=B.values(vP),
+             vdphi=B.gradients(vP), centre=X.mean(axis=1))
+    # per surface: physical quadrature points in the left element's frame
+    sid = np.flatnonzero(prob.active)
+    L = prob.surf_elems[sid, 0]
+    R = prob.surf_elems[sid, 1]
+    XL = X[L]
+    sv = prob.surf_verts[sid]
+    nv = NVERT[kind]
+    corners = []
+    for m in range(sv.shape[1]):
+        k = np.argmax(prob.elem_verts[L, :nv] == sv[:, m:m + 1], axis=1)
+        corners.append(XL[np.arange(len(sid)), k])
+    corners = np.stack(corners, axis=1)                  # (s, w, d)
+    if kind == "tet":
+        xg = np.einsum("gm,smd->sgd", fP, corners)
+        nrm = np.cross(corners[:, 1] - corners[:, 0], corners[:, 2] - corners[:, 0])
+        meas = 0.5 * np.linalg.norm(nrm, axis=1)
+    else:
+        t = fP[:, 0]
+        xg = corners[:, None, 0] + t[None, :, None] * (corners[:, None, 1] - corners[:, None, 0])
+        tv = corners[:, 1] - corners[:, 0]
+        nrm = np.stack([tv[:, 1], -tv[:, 0]], axis=1)
+        meas = np.linalg.norm(tv, axis=1)
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    out = ((corners.mean(axis=1) - c["centre"][L]) * nrm).sum(1) < 0
+    nrm[out] *= -1
+    xiL = _to_ref(Jinv[L], X[L, 0], xg, prob.period, c["centre"][L])
+    phiL = B.values(xiL.reshape(-1, xiL.shape[-1])).reshape(len(sid), len(fW), -1)
+    inner = R >= 0
+    phiR = np.zeros_like(phiL)
+    if inner.any():
+        xiR = _to_ref(Jinv[R[inner]], X[R[inner], 0], xg[inner], prob.period,
+                      c["centre"][R[inner]])
+        phiR[inner] = B.values(xiR.reshape(-1, xiR.shape[-1])).reshape(inner.sum(), len(fW), -1)
+    c.update(sid=sid, L=L, R=R, n=nrm, meas=meas, phiL=phiL, phiR=phiR,
+             col=prob.colors[sid])
+    return c
+
+
+def volume_term(prob: Problem, U: np.ndarray) -> np.ndarray:
+    """U (ne, neq, nb) -> volume contribution (ne, neq, nb)."""
+    c = setup(prob)
+    Uq = np.einsum("qj,ekj->eqk", c["vphi"], U)
+    F = prob.physics.flux(Uq)                                  # (e, q, d, k)
+    Ft = np.einsum("erd,eqdk->eqrk", c["Jinv"], F)             # contravariant
+    return np.einsum("q,rqj,eqrk->ekj", c["vW"], c["vdphi"], Ft)
+
+
+def surface_contributions(prob: Problem, U: np.ndarray, sel=None):
+    """Per-surface (left, right) contributions for the selected entries."""
+    c = setup(prob)
+    sel = np.arange(len(c["sid"])) if sel is None else sel
+    L, R = c["L"][sel], c["R"][sel]
+    UL = np.einsum("sgj,skj->sgk", c["phiL"][sel], U[L])
+    inner = R >= 0
+    UR = np.empty_like(UL)
+    UR[inner] = np.einsum("sgj,skj->sgk", c["phiR"][sel][inner], U[R[inner]])
+    ff = np.asarray(prob.physics.farfield, dtype=np.float64)
+    UR[~inner] = ff[None, :]
+    n = c["n"][sel][:, None, :]
+    Fh = prob.physics.numerical_flux(UL, UR, np.broadcast_to(n, UL.shape[:2] + n.shape[-1:]))
+    wF = c["fW"][None, :, None] * Fh                            # (s, g, k)
+    sL = c["meas"][sel] / np.abs(c["det"][L])
+    cl = -sL[:, None, None] * np.einsum("sgk,sgj->skj", wF, c["phiL"][sel])
+    cr = np.zeros_like(cl)
+    if inner.any():
+        sR = c["meas"][sel][inner] / np.abs(c["det"][R[inner]])
+        cr[inner] = sR[:, None, None] * np.einsum("sgk,sgj->skj", wF[inner], c["phiR"][sel][inner])
+    return L, R, cl, cr
+
+
+def rhs(prob: Problem, U: np.ndarray) -> np.ndarray:
+    """Eq. (2): volume, then surfaces color by color (Algorithm 1)."""
+    c = setup(prob)
+    Rr = volume_term(prob, U)
+    for color in range(1, prob.n_colors + 1):
+        sel = np.flatnonzero(c["col"] == color)
+        if not len(sel):
+            continue
+        L, R, cl, cr = surface_contributions(prob, U, sel)
+        Rr[L] += cl                        # race free: one surface per element per color
+        inner = R >= 0
+        Rr[R[inner]] += cr[inner]
+    return Rr
+
+
+def rhs_buffered_order(prob: Problem, U: np.ndarray) -> np.ndarray:
+    """Same operator, accumulated through a 2*ns buffer (for the variant)."""
+    c = setup(prob)
+    Rr = volume_term(prob, U)
+    L, R, cl, cr = surface_contributions(prob, U)
+    np.add.at(Rr, L, cl)
+    inner = R >= 0
+    np.add.at(Rr, R[inner], cr[inner])
+    return Rr
+
+
+def ssprk3(prob: Problem, U: np.ndarray, dt: float, steps: int = 1) -> np.ndarray:
+    U = U.copy()
+    for _ in range(steps):
+        U1 = U + dt * rhs(prob, U)
+        U2 = 0.75 * U + 0.25 * (U1 + dt * rhs(prob, U1))
+        U = U / 3.0 + 2.0 / 3.0 * (U2 + dt * rhs(prob, U2))
+    return U
+
+
+def project(prob: Problem, fn) -> np.ndarray:
+    """L2 projection of fn(x (n, d)) -> (n, neq) onto the basis."""
+    c = setup(prob)
+    vP, vW = vol_rule(prob.kind, prob.p + 1)
+    phi = c["B"].values(vP)
+    x = c["X"][:, 0][:, None, :] + np.einsum("erd,qd->eqr",
+                                              np.linalg.inv(c["Jinv"]), vP)
+    vals = fn(x.reshape(-1, x.shape[-1])).reshape(x.shape[0], x.shape[1], -1)
+    return np.einsum("q,qj,eqk->ekj", vW, phi, vals) / (vW.sum() * 0 + 1.0)
+
+
+def mass_weights(prob: Problem) -> np.ndarray:
+    """|det J_e| * integral(phi_0): element mass of mode-0 coefficient."""
+    c = setup(prob)
+    vP, vW = vol_rule(prob.kind, prob.p + 1)
+    phi0 = c["B"].values(vP)[:, 0]
+    return np.abs(c["det"]) * np.sum(vW * phi0)
+
+
+def problem_from(desc: dict) -> Problem:
+    """Build an oracle Problem from ``DGOperator.oracle_problem()``."""
+    phys = Physics(desc["physics"], desc["dim"], gamma=desc["gamma"],
+                   velocity=tuple(desc["velocity"]), farfield=tuple(desc["farfield"]))
+    return Problem(desc["kind"], desc["p"], phys, desc["vertices"], desc["elem_verts"],
+                   desc["surf_verts"], desc["surf_elems"], desc["colors"],
+                   desc["n_colors"], desc["active"], desc["period"])
+
+
+def term_scale(prob: Problem, U: np.ndarray) -> float:
+    """Magnitude of the largest term of Eq. (2) (the volume integral),
+    the denominator of the parity tolerance: near free stream the residual
+    is a small difference of O(term) quantities, so rounding differences
+    scale with the terms, not with the residual."""
+    return float(np.abs(volume_term(prob, U)).max())
+
+
+def rel_error(got: np.ndarray, want: np.ndarray, prob: Problem, U: np.ndarray) -> float:
+    scale = max(float(np.abs(want).max()), term_scale(prob, U), 1e-300)
+    return float(np.abs(got - want).max()) / scale

@@ -51,7 +51,7 @@ class DGDesc(C.Structure):
         ("group_bounds", C.c_void_p), ("surf_left", C.c_void_p),
         ("surf_right", C.c_void_p), ("surf_code", C.c_void_p),
         ("surf_geom", C.c_void_p), ("elem_jinv", C.c_void_p),
-        ("elem_surfs", C.c_void_p), ("elem_side_of", C.c_void_p),
+        ("elem_slot_ptr", C.c_void_p), ("elem_slots", C.c_void_p),
         ("n_face_codes", C.c_int), ("n_face_q", C.c_int),
         ("n_vol_q", C.c_int), ("n_basis", C.c_int),
         ("face_phi", C.c_void_p), ("face_w", C.c_void_p),
@@ -92,6 +92,8 @@ _SIGS = {
     "mc_dg_rhs": (C.c_int, [_P, _P, _P, C.c_int, _P]),
     "mc_dg_rk_stage": (C.c_int, [_P, _P, _P, _P, C.c_double, C.c_double,
                                  C.c_double, _P]),
+    "mc_dg_color_pass": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_double,
+                                   C.c_double, C.c_double, _P]),
     "mc_dg_ssprk3": (C.c_int, [_P, _P, _P, C.c_double, C.c_int, _P]),
     "mc_dg_ssprk3_host": (C.c_int, [_P, _P, C.c_double, C.c_int]),
 }

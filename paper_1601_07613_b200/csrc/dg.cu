@@ -1,12 +1,269 @@
-// placeholder, replaced by the DG kernels
+// C ABI of the DG operator: handle creation (upload of the color-major
+// surface list, element geometry and reference tables), the colored /
+// buffered / atomic RHS strategies and the fused SSP-RK3 stepper.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dg_ops.h"
 #include "mc_internal.h"
-extern "C" {
-MC_API int mc_dg_create(const mc_dg_desc*, mc_dg**) { return mc_fail(MC_EUNSUPPORTED, "todo"); }
-MC_API int mc_dg_destroy(mc_dg*) { return 0; }
-MC_API int64_t mc_dg_block_stride(const mc_dg*) { return 0; }
-MC_API int64_t mc_dg_buffer_bytes(const mc_dg*) { return 0; }
-MC_API int mc_dg_rhs(mc_dg*, const double*, double*, int, void*) { return 9; }
-MC_API int mc_dg_rk_stage(mc_dg*, double*, const double*, double*, double, double, double, void*) { return 9; }
-MC_API int mc_dg_ssprk3(mc_dg*, double*, double*, double, int, void*) { return 9; }
-MC_API int mc_dg_ssprk3_host(mc_dg*, double*, double, int) { return 9; }
+
+using mcdg::Ops;
+
+struct mc_dg {
+  Ops* ops = nullptr;
+  mcdg::View view{};
+  int n_colors = 0;
+  std::vector<int64_t> bounds;
+  int64_t ne = 0, ng = 0, ns = 0, stride = 0;
+  // device allocations
+  int32_t *d_left = nullptr, *d_right = nullptr, *d_slots = nullptr;
+  uint32_t* d_code = nullptr;
+  double *d_geom = nullptr, *d_jinv = nullptr, *d_tables = nullptr;
+  int64_t* d_slot_ptr = nullptr;
+  double* d_buffer = nullptr;      // 2*ns blocks (buffered strategy)
+  double* d_host_U = nullptr;      // host path scratch: U, U0, R
+  cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+#define DG_TRY(expr)                                                                    \
+  do {                                                                                  \
+    cudaError_t e__ = (expr);                                                           \
+    if (e__ != cudaSuccess)                                                             \
+      return mc_fail(MC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e__));    \
+  } while (0)
+
+template <class T>
+cudaError_t upload(T** dst, const T* src, int64_t count) {
+  if (count <= 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), sizeof(T) * size_t(count));
+  if (e != cudaSuccess) return e;
+  if (src) return cudaMemcpy(*dst, src, sizeof(T) * size_t(count), cudaMemcpyHostToDevice);
+  return cudaSuccess;
 }
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int colored_pass(mc_dg* h, double* U, double* R, const mcdg::RK* rk, cudaStream_t s) {
+  for (int c = 1; c <= h->n_colors; ++c) {
+    const int64_t b = h->bounds[c - 1], e = h->bounds[c];
+    if (e == b) continue;
+    int64_t need = (e - b + h->ops->neq) / 1;  // surfaces
+    int grid = h->ops->grid_colored;
+    // do not launch more warps than surface tiles
+    const int spw = 32 / (2 * h->ops->neq);
+    const int64_t tiles = (e - b + spw - 1) / spw;
+    const int64_t warps_per_block = mcdg::kThreads / 32;
+    const int64_t max_blocks = (tiles + warps_per_block - 1) / warps_per_block;
+    if (grid > max_blocks) grid = int(max_blocks);
+    (void)need;
+    DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, grid, s));
+  }
+  return MC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
+  if (!d || !out) return mc_fail(MC_EINVAL, "null argument");
+  *out = nullptr;
+  Ops* ops = nullptr;
+  if (d->kind == MC_KIND_TRI) ops = mcdg::ops_tri(d->physics, d->degree);
+  else if (d->kind == MC_KIND_QUAD) ops = mcdg::ops_quad(d->physics, d->degree);
+  else if (d->kind == MC_KIND_TET) ops = mcdg::ops_tet(d->physics, d->degree);
+  if (!ops)
+    return mc_fail(MC_EUNSUPPORTED, "no sm_100a kernel compiled for kind " +
+                                        std::to_string(d->kind) + " physics " +
+                                        std::to_string(d->physics) + " degree " +
+                                        std::to_string(d->degree));
+  if (d->n_face_codes != ops->ncodes || d->n_face_q != ops->nqf || d->n_vol_q != ops->nqv ||
+      d->n_basis != ops->np)
+    return mc_fail(MC_EINVAL, "reference tables do not match the compiled kernel");
+  if (d->n_elements <= 0 || d->n_surfaces < 0 || d->n_colors < 1 || d->n_ghosts < 0)
+    return mc_fail(MC_EINVAL, "bad DG sizes");
+  if (d->n_elements + d->n_ghosts >= (int64_t(1) << 31) || d->n_surfaces >= (int64_t(1) << 31))
+    return mc_fail(MC_EINVAL, "mesh too large for 32-bit ids");
+  if (d->group_bounds[0] != 0 || d->group_bounds[d->n_colors] != d->n_surfaces)
+    return mc_fail(MC_EINVAL, "group bounds do not cover the surface list");
+  for (int c = 1; c <= d->n_colors; ++c)
+    if (d->group_bounds[c] < d->group_bounds[c - 1])
+      return mc_fail(MC_EINVAL, "group bounds must be non-decreasing");
+  const int64_t nall = d->n_elements + d->n_ghosts;
+  for (int64_t s = 0; s < d->n_surfaces; ++s) {
+    const int32_t l = d->surf_left[s], r = d->surf_right[s];
+    if (l < 0 || l >= d->n_elements || r >= nall)
+      return mc_fail(MC_EINVAL, "surface " + std::to_string(s) + " has a bad element id");
+  }
+  if (ops->init) {
+    cudaError_t e = ops->init(ops);
+    ops->init = nullptr;  // once per process
+    if (e != cudaSuccess)
+      return mc_fail(MC_ECUDA, std::string("kernel setup: ") + cudaGetErrorString(e));
+  }
+  auto h = new mc_dg();
+  h->ops = ops;
+  h->n_colors = d->n_colors;
+  h->bounds.assign(d->group_bounds, d->group_bounds + d->n_colors + 1);
+  h->ne = d->n_elements;
+  h->ng = d->n_ghosts;
+  h->ns = d->n_surfaces;
+  const int64_t w = int64_t(ops->neq) * ops->np;
+  h->stride = (w + 3) / 4 * 4;  // 32-byte aligned element blocks
+  const int dim = ops->dim;
+  std::vector<double> tables(ops->table_size);
+  {
+    double* t = tables.data();
+    const int64_t nf = int64_t(ops->ncodes) * ops->nqf * ops->np;
+    std::memcpy(t, d->face_phi, sizeof(double) * nf);
+    t += nf;
+    std::memcpy(t, d->face_w, sizeof(double) * ops->nqf);
+    t += ops->nqf;
+    std::memcpy(t, d->vol_phi, sizeof(double) * ops->nqv * ops->np);
+    t += ops->nqv * ops->np;
+    std::memcpy(t, d->vol_dphi, sizeof(double) * dim * ops->nqv * ops->np);
+    t += dim * ops->nqv * ops->np;
+    std::memcpy(t, d->vol_w, sizeof(double) * ops->nqv);
+  }
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = upload(&h->d_left, d->surf_left, h->ns);
+  if (e == cudaSuccess) e = upload(&h->d_right, d->surf_right, h->ns);
+  if (e == cudaSuccess) e = upload(&h->d_code, d->surf_code, h->ns);
+  if (e == cudaSuccess) e = upload(&h->d_geom, d->surf_geom, h->ns * (dim + 2));
+  if (e == cudaSuccess) e = upload(&h->d_jinv, d->elem_jinv, nall * dim * dim);
+  if (e == cudaSuccess) e = upload(&h->d_tables, tables.data(), int64_t(tables.size()));
+  if (e == cudaSuccess && d->elem_slot_ptr) e = upload(&h->d_slot_ptr, d->elem_slot_ptr, h->ne + 1);
+  if (e == cudaSuccess && d->elem_slots)
+    e = upload(&h->d_slots, d->elem_slots, d->elem_slot_ptr[h->ne]);
+  if (e != cudaSuccess) {
+    mc_dg_destroy(h);
+    return mc_fail(MC_ENOMEM, std::string("DG upload: ") + cudaGetErrorString(e));
+  }
+  mcdg::View& v = h->view;
+  v.left = h->d_left;
+  v.right = h->d_right;
+  v.code = h->d_code;
+  v.geom = h->d_geom;
+  v.jinv = h->d_jinv;
+  v.tables = h->d_tables;
+  v.slot_ptr = h->d_slot_ptr;
+  v.slots = h->d_slots;
+  v.n_elements = h->ne;
+  v.n_surfaces = h->ns;
+  v.stride = h->stride;
+  v.prm.gamma = d->gamma;
+  for (int k = 0; k < 3; ++k) v.prm.vel[k] = d->velocity[k];
+  for (int k = 0; k < 5; ++k) v.prm.ff[k] = d->farfield[k];
+  *out = h;
+  return MC_OK;
+}
+
+MC_API int mc_dg_destroy(mc_dg* h) {
+  if (!h) return MC_OK;
+  cudaFree(h->d_left);
+  cudaFree(h->d_right);
+  cudaFree(h->d_code);
+  cudaFree(h->d_geom);
+  cudaFree(h->d_jinv);
+  cudaFree(h->d_tables);
+  cudaFree(h->d_slot_ptr);
+  cudaFree(h->d_slots);
+  cudaFree(h->d_buffer);
+  cudaFree(h->d_host_U);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return MC_OK;
+}
+
+MC_API int64_t mc_dg_block_stride(const mc_dg* h) { return h ? h->stride : -1; }
+
+MC_API int64_t mc_dg_buffer_bytes(const mc_dg* h) {
+  return h ? 2 * h->ns * h->stride * int64_t(sizeof(double)) : -1;
+}
+
+MC_API int mc_dg_rhs(mc_dg* h, const double* U, double* R, int strategy, void* stream) {
+  if (!h || !U || !R) return mc_fail(MC_EINVAL, "null argument");
+  cudaStream_t s = as_stream(stream);
+  double* Um = const_cast<double*>(U);  // the non-RK colored pass never writes U
+  if (strategy == MC_DG_COLORED) return colored_pass(h, Um, R, nullptr, s);
+  if (strategy != MC_DG_BUFFERED && strategy != MC_DG_ATOMIC)
+    return mc_fail(MC_EINVAL, "unknown strategy");
+  int gv = h->ops->grid_volume;
+  DG_TRY(h->ops->volume(h->view, U, R, gv, s));
+  if (strategy == MC_DG_ATOMIC) {
+    if (h->ns) DG_TRY(h->ops->uncolored(h->view, U, R, true, h->ops->grid_uncolored, s));
+    return MC_OK;
+  }
+  if (!h->d_slot_ptr) return mc_fail(MC_EINVAL, "buffered strategy needs the element slot CSR");
+  if (!h->d_buffer) DG_TRY(cudaMalloc(&h->d_buffer, size_t(mc_dg_buffer_bytes(h)) + 16));
+  if (h->ns) DG_TRY(h->ops->uncolored(h->view, U, h->d_buffer, false, h->ops->grid_uncolored, s));
+  DG_TRY(h->ops->gather(h->view, h->d_buffer, R, s));
+  return MC_OK;
+}
+
+MC_API int mc_dg_rk_stage(mc_dg* h, double* U, const double* U0, double* R, double a, double b,
+                          double dt, void* stream) {
+  if (!h || !U || !R || (a != 0.0 && !U0)) return mc_fail(MC_EINVAL, "null argument");
+  mcdg::RK rk{const_cast<double*>(U0), a, b, dt, 0};
+  return colored_pass(h, U, R, &rk, as_stream(stream));
+}
+
+MC_API int mc_dg_color_pass(mc_dg* h, int color, double* U, double* U0, double* R, int rk_mode,
+                            double a, double b, double dt, void* stream) {
+  if (!h || !U || !R) return mc_fail(MC_EINVAL, "null argument");
+  if (color < 1 || color > h->n_colors) return mc_fail(MC_EINVAL, "bad color");
+  const int64_t bb = h->bounds[color - 1], e = h->bounds[color];
+  if (e == bb) return MC_OK;
+  const int spw = 32 / (2 * h->ops->neq);
+  const int64_t tiles = (e - bb + spw - 1) / spw;
+  const int64_t max_blocks = (tiles + mcdg::kThreads / 32 - 1) / (mcdg::kThreads / 32);
+  int grid = h->ops->grid_colored;
+  if (grid > max_blocks) grid = int(max_blocks);
+  if (rk_mode == 0) {
+    DG_TRY(h->ops->colored(h->view, U, R, nullptr, bb, e, grid, as_stream(stream)));
+  } else {
+    if (!U0) return mc_fail(MC_EINVAL, "RK pass needs U0");
+    mcdg::RK rk{U0, a, b, dt, rk_mode == 2 ? 1 : 0};
+    DG_TRY(h->ops->colored(h->view, U, R, &rk, bb, e, grid, as_stream(stream)));
+  }
+  return MC_OK;
+}
+
+MC_API int mc_dg_ssprk3(mc_dg* h, double* U, double* work, double dt, int n_steps,
+                        void* stream) {
+  if (!h || !U || !work || n_steps < 0) return mc_fail(MC_EINVAL, "bad argument");
+  cudaStream_t s = as_stream(stream);
+  double* U0 = work;
+  double* R = work + (h->ne + h->ng) * h->stride;
+  for (int step = 0; step < n_steps; ++step) {
+    // stage 1 saves U0 := U in its last-touch pass (no separate copy)
+    mcdg::RK r1{U0, 0.0, 1.0, dt, 1};
+    if (int rc = colored_pass(h, U, R, &r1, s)) return rc;
+    mcdg::RK r2{U0, 0.75, 0.25, dt, 0};
+    if (int rc = colored_pass(h, U, R, &r2, s)) return rc;
+    mcdg::RK r3{U0, 1.0 / 3.0, 2.0 / 3.0, dt, 0};
+    if (int rc = colored_pass(h, U, R, &r3, s)) return rc;
+  }
+  return MC_OK;
+}
+
+MC_API int mc_dg_ssprk3_host(mc_dg* h, double* U_host, double dt, int n_steps) {
+  if (!h || !U_host) return mc_fail(MC_EINVAL, "null argument");
+  const int64_t nblk = (h->ne + h->ng) * h->stride;
+  if (!h->d_host_U) DG_TRY(cudaMalloc(&h->d_host_U, sizeof(double) * size_t(3 * nblk)));
+  if (!h->stream) DG_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  DG_TRY(cudaMemcpyAsync(h->d_host_U, U_host, sizeof(double) * nblk, cudaMemcpyHostToDevice,
+                         h->stream));
+  if (int rc = mc_dg_ssprk3(h, h->d_host_U, h->d_host_U + nblk, dt, n_steps, h->stream)) return rc;
+  DG_TRY(cudaMemcpyAsync(U_host, h->d_host_U, sizeof(double) * h->ne * h->stride,
+                         cudaMemcpyDeviceToHost, h->stream));
+  DG_TRY(cudaStreamSynchronize(h->stream));
+  return MC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,18 @@
+// Kernel instantiations for tet elements (advection and Euler).
+#include "dg_ops.h"
+
+namespace mcdg {
+
+Ops* ops_tet(int phys, int p) {
+  switch (phys * 16 + p) {
+    case ADV * 16 + 1: return Instance<TET, ADV, 1>::ops();
+    case EULER * 16 + 1: return Instance<TET, EULER, 1>::ops();
+    case ADV * 16 + 2: return Instance<TET, ADV, 2>::ops();
+    case EULER * 16 + 2: return Instance<TET, EULER, 2>::ops();
+    case ADV * 16 + 3: return Instance<TET, ADV, 3>::ops();
+    case EULER * 16 + 3: return Instance<TET, EULER, 3>::ops();
+    default: return nullptr;
+  }
+}
+
+}  // namespace mcdg

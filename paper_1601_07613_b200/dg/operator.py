@@ -1,0 +1,329 @@
+"""DG operator: the RHS / SSP-RK API the north star asks for.
+
+``DGOperator(mesh, coloring, degree, physics)`` builds, once on the host:
+the color-major renumbering (``reorder.build_plan`` + ``apply_plan``,
+reference reorder.py:64-167), the DG surface list and element geometry
+(``dg.layout``), the reference-element tables (``dg.basis``) — and uploads
+them through ``mc_dg_create``.  Every evaluation then runs on the B200:
+
+* ``rhs(U, strategy)`` — Eq. (2) by Algorithm 1
+  (PAPER.md:64-82): one launch per color, no atomics, no buffer
+  (``strategy="colored"``), or the paper's comparison variants
+  ``"buffered"`` (2*ns slot buffer + gather) and ``"atomic"``;
+* ``ssprk3(U, dt, steps)`` — SSP-RK3 with the volume integral fused into
+  each element's first color pass and the stage update into its last.
+
+Host arrays are in the caller's (original) element order, shape
+(ne, n_equations, n_basis); device tensors (``*_device``) use the internal
+layout: renumbered elements, blocks of ``stride`` doubles (32-byte padded).
+There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .. import _native
+from ..amr import RefinedMesh
+from ..coloring import SurfaceColoring, color
+from ..mesh import ElementKind, Mesh
+from ..reorder import ReorderingPlan, apply_plan, build_plan
+from .basis import DIM, REF_MEASURE, evaluate_basis, reference_tables, volume_rule
+from .layout import build_surface_list, mesh_kind, unwrapped_element_coords
+
+_KIND_CODE = {ElementKind.TRIANGLE: 0, ElementKind.QUAD: 1, ElementKind.TET: 2}
+_STRATEGY = {"colored": 0, "buffered": 1, "atomic": 2}
+
+
+def default_freestream(dim: int, gamma: float = 1.4):
+    rho, p = 1.0, 1.0
+    vel = (0.3, 0.2, 0.1)[:dim]
+    E = p / (gamma - 1.0) + 0.5 * rho * sum(v * v for v in vel)
+    return (rho, *[rho * v for v in vel], E)
+
+
+def ordering_plan(mesh: Mesh, coloring: SurfaceColoring, ordering: str) -> ReorderingPlan:
+    """The three layouts of the paper's Table 7:
+    "reorder" = element renumbering + edge reordering (build_plan),
+    "renumber" = element renumbering only, surfaces grouped by color in
+    original id order, "none" = original numbering, surfaces grouped by
+    color."""
+    colors = np.asarray(coloring.colors)
+    full = build_plan(mesh, coloring)
+    if ordering == "reorder":
+        return full
+    order = np.argsort(colors, kind="stable")
+    sp = np.empty(mesh.n_surfaces, dtype=np.int64)
+    sp[order] = np.arange(mesh.n_surfaces)
+    ep = full.element_perm if ordering == "renumber" else np.arange(mesh.n_elements)
+    if ordering not in ("renumber", "none"):
+        raise ValueError(f"unknown ordering {ordering!r}")
+    return ReorderingPlan(np.asarray(ep, dtype=np.int64).copy(), sp, full.group_bounds,
+                          full.n_interior_first, full.used_fallback)
+
+
+class DGOperator:
+    def __init__(self, mesh, coloring: SurfaceColoring | None = None, degree: int = 1,
+                 physics: str = "euler", *, period=None, gamma: float = 1.4,
+                 velocity=(1.0, 0.5, 0.25), farfield=None, ordering: str = "reorder"):
+        mortars = None
+        if isinstance(mesh, RefinedMesh):
+            mortars = mesh.hanging_array()
+            mesh = mesh.mesh
+        self.mesh = mesh
+        if coloring is None:
+            coloring, _ = color(mesh)
+        self.coloring = coloring
+        self.kind = mesh_kind(mesh)
+        self.dim = DIM[self.kind]
+        self.degree = int(degree)
+        self.physics = physics
+        if physics not in ("advection", "euler"):
+            raise ValueError(f"unknown physics {physics!r}")
+        self.n_equations = 1 if physics == "advection" else self.dim + 2
+        self.gamma = float(gamma)
+        self.velocity = tuple(float(v) for v in velocity) + (0.0,) * (3 - len(velocity))
+        if farfield is None:
+            farfield = (0.0,) if physics == "advection" else default_freestream(self.dim, gamma)
+        self.farfield = tuple(float(x) for x in farfield)
+        if len(self.farfield) != self.n_equations:
+            raise ValueError("far-field state needs one value per equation")
+        self.period = period
+        self.ordering = ordering
+
+        self.plan = ordering_plan(mesh, coloring, ordering)
+        self.layout_mesh, lcol = apply_plan(mesh, coloring, self.plan)
+        self.layout_coloring = lcol
+        if mortars is not None and len(mortars):
+            mortars = self.plan.surface_perm[mortars]
+        self.surfaces = build_surface_list(self.layout_mesh, lcol.colors, lcol.n_colors,
+                                           period=period, mortars=mortars)
+        self.mortars = mortars
+        self.tables = reference_tables(self.kind, self.degree)
+        self.n_basis = self.tables.n_basis
+        self.n_elements = mesh.n_elements
+        self._create()
+
+    # ---------------------------------------------------------- native
+    def _create(self):
+        lib = _native.lib()
+        _native.require_device()
+        sl, t = self.surfaces, self.tables
+        keep = dict(
+            bounds=np.ascontiguousarray(sl.bounds, dtype=np.int64),
+            left=np.ascontiguousarray(sl.left), right=np.ascontiguousarray(sl.right),
+            code=np.ascontiguousarray(sl.code), geom=np.ascontiguousarray(sl.geom),
+            jinv=np.ascontiguousarray(sl.jinv.reshape(-1)),
+            ptr=np.ascontiguousarray(sl.slot_ptr, dtype=np.int64),
+            slots=np.ascontiguousarray(sl.slots, dtype=np.int32),
+            fphi=np.ascontiguousarray(t.face_phi), fw=np.ascontiguousarray(t.face_w),
+            vphi=np.ascontiguousarray(t.vol_phi), vdphi=np.ascontiguousarray(t.vol_dphi),
+            vw=np.ascontiguousarray(t.vol_w))
+        d = _native.DGDesc()
+        d.kind = _KIND_CODE[self.kind]
+        d.physics = 0 if self.physics == "advection" else 1
+        d.degree = self.degree
+        d.n_colors = sl.n_colors
+        d.n_elements = sl.n_elements
+        d.n_ghosts = sl.n_ghosts
+        d.n_surfaces = sl.n_surfaces
+        P = _native.ptr
+        d.group_bounds, d.surf_left, d.surf_right = P(keep["bounds"]), P(keep["left"]), P(keep["right"])
+        d.surf_code, d.surf_geom, d.elem_jinv = P(keep["code"]), P(keep["geom"]), P(keep["jinv"])
+        d.elem_slot_ptr, d.elem_slots = P(keep["ptr"]), P(keep["slots"])
+        d.n_face_codes, d.n_face_q = t.n_codes, len(t.face_w)
+        d.n_vol_q, d.n_basis = len(t.vol_w), t.n_basis
+        d.face_phi, d.face_w = P(keep["fphi"]), P(keep["fw"])
+        d.vol_phi, d.vol_dphi, d.vol_w = P(keep["vphi"]), P(keep["vdphi"]), P(keep["vw"])
+        d.gamma = self.gamma
+        for k in range(3):
+            d.velocity[k] = self.velocity[k]
+        ff = list(self.farfield) + [0.0] * (5 - len(self.farfield))
+        for k in range(5):
+            d.farfield[k] = ff[k]
+        h = _native.C.c_void_p()
+        _native.check(lib.mc_dg_create(_native.C.byref(d), _native.C.byref(h)))
+        self._lib = lib
+        self._h = h
+        self.stride = int(lib.mc_dg_block_stride(h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.mc_dg_destroy(h)
+            self._h = None
+
+    # ----------------------------------------------------- layout maps
+    @property
+    def n_colors(self) -> int:
+        return self.surfaces.n_colors
+
+    @property
+    def n_surfaces(self) -> int:
+        return self.surfaces.n_surfaces
+
+    def block_width(self) -> int:
+        return self.n_equations * self.n_basis
+
+    def to_internal(self, U: np.ndarray) -> np.ndarray:
+        """(ne, neq, nb) user order -> (ne, stride) renumbered, padded."""
+        U = np.asarray(U, dtype=np.float64).reshape(self.n_elements, -1)
+        out = np.zeros((self.n_elements, self.stride))
+        out[self.plan.element_perm, : self.block_width()] = U
+        return out
+
+    def from_internal(self, B: np.ndarray) -> np.ndarray:
+        B = np.asarray(B).reshape(self.n_elements, self.stride)
+        return B[self.plan.element_perm, : self.block_width()].reshape(
+            self.n_elements, self.n_equations, self.n_basis).copy()
+
+    def empty_device(self):
+        import torch
+        return torch.zeros((self.n_elements, self.stride), dtype=torch.float64, device="cuda")
+
+    def to_device(self, U: np.ndarray):
+        import torch
+        return torch.from_numpy(self.to_internal(U)).to("cuda")
+
+    def from_device(self, t) -> np.ndarray:
+        import torch
+        torch.cuda.current_stream().synchronize()
+        return self.from_internal(t.cpu().numpy())
+
+    # ------------------------------------------------------- evaluation
+    def rhs_device(self, U_dev, R_dev, strategy: str = "colored", stream=None) -> None:
+        _native.check(self._lib.mc_dg_rhs(self._h, _native.ptr(U_dev), _native.ptr(R_dev),
+                                          _STRATEGY[strategy], _native.stream_ptr(stream)))
+
+    def rk_stage_device(self, U_dev, U0_dev, R_dev, a, b, dt, stream=None) -> None:
+        _native.check(self._lib.mc_dg_rk_stage(
+            self._h, _native.ptr(U_dev), _native.ptr(U0_dev), _native.ptr(R_dev),
+            float(a), float(b), float(dt), _native.stream_ptr(stream)))
+
+    def color_pass_device(self, color: int, U_dev, U0_dev, R_dev, rk_mode: int = 0,
+                          a: float = 0.0, b: float = 1.0, dt: float = 0.0, stream=None) -> None:
+        _native.check(self._lib.mc_dg_color_pass(
+            self._h, int(color), _native.ptr(U_dev), _native.ptr(U0_dev), _native.ptr(R_dev),
+            int(rk_mode), float(a), float(b), float(dt), _native.stream_ptr(stream)))
+
+    def work_device(self):
+        import torch
+        return torch.zeros((2, self.n_elements, self.stride), dtype=torch.float64, device="cuda")
+
+    def ssprk3_device(self, U_dev, work_dev, dt: float, steps: int = 1, stream=None) -> None:
+        _native.check(self._lib.mc_dg_ssprk3(self._h, _native.ptr(U_dev), _native.ptr(work_dev),
+                                             float(dt), int(steps), _native.stream_ptr(stream)))
+
+    def rhs(self, U: np.ndarray, strategy: str = "colored") -> np.ndarray:
+        import torch
+        Ud = self.to_device(U)
+        Rd = torch.zeros_like(Ud)
+        self.rhs_device(Ud, Rd, strategy)
+        return self.from_device(Rd)
+
+    def ssprk3(self, U: np.ndarray, dt: float, steps: int = 1) -> np.ndarray:
+        """End to end through host buffers (``mc_dg_ssprk3_host``)."""
+        B = np.ascontiguousarray(self.to_internal(U))
+        _native.check(self._lib.mc_dg_ssprk3_host(self._h, _native.ptr(B), float(dt), int(steps)))
+        return self.from_internal(B)
+
+    def ssprk3_host_internal(self, B: np.ndarray, dt: float, steps: int = 1) -> None:
+        """In-place SSP-RK3 on a host array already in the internal layout
+        (pinned or pageable); the bench's end-to-end leg."""
+        _native.check(self._lib.mc_dg_ssprk3_host(self._h, _native.ptr(B), float(dt), int(steps)))
+
+    # ------------------------------------------------------------ setup
+    def element_coords(self) -> np.ndarray:
+        return unwrapped_element_coords(self.mesh, self.period)
+
+    def project(self, fn) -> np.ndarray:
+        """L2 projection of fn(x (n, dim)) -> (n, neq) (user order)."""
+        X = self.element_coords()
+        pts, w = volume_rule(self.kind, self.degree + 1)
+        phi, _ = evaluate_basis(self.kind, self.degree, pts)
+        if self.kind is ElementKind.QUAD:
+            J = np.stack([X[:, 1] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)
+        else:
+            J = np.stack([X[:, r + 1] - X[:, 0] for r in range(self.dim)], axis=2)
+        out = np.empty((self.n_elements, self.n_equations, self.n_basis))
+        chunk = 1 << 16
+        for a in range(0, self.n_elements, chunk):
+            b = min(a + chunk, self.n_elements)
+            x = X[a:b, 0][:, None, :] + np.einsum("erk,qk->eqr", J[a:b], pts)
+            vals = fn(x.reshape(-1, self.dim)).reshape(b - a, len(w), self.n_equations)
+            out[a:b] = np.einsum("q,qj,eqk->ekj", w, phi, vals)
+        return out
+
+    def domain(self):
+        X = self.element_coords().reshape(-1, self.dim)
+        lo, hi = X.min(axis=0), X.max(axis=0)
+        if self.period is not None:
+            for d, L in enumerate(self.period):
+                if L:
+                    lo[d], hi[d] = 0.0, float(L)
+        return lo, hi
+
+    def initial_state(self, name: str = "wave") -> np.ndarray:
+        lo, hi = self.domain()
+        ext = np.maximum(hi - lo, 1e-12)
+        if self.physics == "advection":
+            def f(x):
+                s = np.sin(2 * np.pi * (x[:, 0] - lo[0]) / ext[0])
+                for d in range(1, self.dim):
+                    s = s * np.cos(2 * np.pi * (x[:, d] - lo[d]) / ext[d])
+                return s[:, None]
+            return self.project(f)
+        ff = np.asarray(self.farfield)
+        rho0 = ff[0]
+        vel = ff[1:1 + self.dim] / rho0
+        p0 = (self.gamma - 1) * (ff[-1] - 0.5 * rho0 * (vel * vel).sum())
+
+        def g(x):
+            if name == "freestream":
+                rho = np.full(len(x), rho0)
+            else:  # smooth density wave carried by the free stream
+                rho = rho0 * (1.0 + 0.2 * np.prod(
+                    [np.sin(2 * np.pi * (x[:, d] - lo[d]) / ext[d]) for d in range(self.dim)],
+                    axis=0))
+            out = np.empty((len(x), self.n_equations))
+            out[:, 0] = rho
+            for d in range(self.dim):
+                out[:, 1 + d] = rho * vel[d]
+            out[:, -1] = p0 / (self.gamma - 1) + 0.5 * rho * (vel * vel).sum()
+            return out
+        return self.project(g)
+
+    def stable_dt(self, cfl: float = 0.1) -> float:
+        """CFL-type step h / (max wave speed * (2p+1))."""
+        detj = np.abs(self.surfaces.detj[: self.n_elements])
+        h = (detj / REF_MEASURE[self.kind]) ** (1.0 / self.dim)
+        ff = np.asarray(self.farfield)
+        if self.physics == "advection":
+            speed = np.linalg.norm(self.velocity[: self.dim]) + 1e-30
+        else:
+            rho = ff[0]
+            vel = ff[1:1 + self.dim] / rho
+            p = (self.gamma - 1) * (ff[-1] - 0.5 * rho * (vel * vel).sum())
+            speed = np.linalg.norm(vel) + np.sqrt(self.gamma * p / rho * 1.3)
+        return float(cfl * h.min() / (speed * (2 * self.degree + 1)))
+
+    # ------------------------------------------------------------ oracle
+    def oracle_problem(self) -> dict:
+        """Plain description (user order) a checker can rebuild the same
+        discretisation from; mortar halves carry their coarse neighbour as
+        right element and full coarse edges are inactive."""
+        m = self.mesh
+        surf_elems = m.surf_elems.copy()
+        active = np.ones(m.n_surfaces, dtype=bool)
+        if self.mortars is not None and len(self.mortars):
+            inv = np.empty_like(self.plan.surface_perm)
+            inv[self.plan.surface_perm] = np.arange(len(inv))
+            mt = inv[self.mortars]
+            for k in (1, 2):
+                surf_elems[mt[:, k], 1] = surf_elems[mt[:, 0], 0]
+            active[mt[:, 0]] = False
+        return dict(kind=self.kind.value, p=self.degree, physics=self.physics, dim=self.dim,
+                    gamma=self.gamma, velocity=self.velocity, farfield=self.farfield,
+                    vertices=m.vertices, elem_verts=m.elem_verts, surf_verts=m.surf_verts,
+                    surf_elems=surf_elems, colors=np.asarray(self.coloring.colors),
+                    n_colors=int(self.coloring.n_colors), active=active, period=self.period)
