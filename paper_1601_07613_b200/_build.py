@@ -58,6 +58,7 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
                "-I", str(PKG.parent / "include"), "-c", str(src), "-o", str(obj)]
         if src.suffix == ".cu":
             cmd[5:5] = ["--expt-relaxed-constexpr"]
+        cmd[5:5] = [f"-D{d}" for d in os.environ.get("MC_DEFINES", "").split() if d]
         jobs.append((src, cmd))
         objs.append(obj)
     procs = [(src, subprocess.Popen(cmd, stdout=subprocess.PIPE,

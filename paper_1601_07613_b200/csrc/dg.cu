@@ -48,20 +48,21 @@ cudaError_t upload(T** dst, const T* src, int64_t count) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+int colored_grid(const mc_dg* h, int64_t n) {
+  // never launch more warps than surface tiles of the color
+  const int64_t tiles = (n + h->ops->spw - 1) / h->ops->spw;
+  const int64_t wpb = h->ops->threads / 32;
+  const int64_t max_blocks = (tiles + wpb - 1) / wpb;
+  int grid = h->ops->grid_colored;
+  if (grid > max_blocks) grid = int(max_blocks);
+  return grid < 1 ? 1 : grid;
+}
+
 int colored_pass(mc_dg* h, double* U, double* R, const mcdg::RK* rk, cudaStream_t s) {
   for (int c = 1; c <= h->n_colors; ++c) {
     const int64_t b = h->bounds[c - 1], e = h->bounds[c];
     if (e == b) continue;
-    int64_t need = (e - b + h->ops->neq) / 1;  // surfaces
-    int grid = h->ops->grid_colored;
-    // do not launch more warps than surface tiles
-    const int spw = 32 / (2 * h->ops->neq);
-    const int64_t tiles = (e - b + spw - 1) / spw;
-    const int64_t warps_per_block = mcdg::kThreads / 32;
-    const int64_t max_blocks = (tiles + warps_per_block - 1) / warps_per_block;
-    if (grid > max_blocks) grid = int(max_blocks);
-    (void)need;
-    DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, grid, s));
+    DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, colored_grid(h, e - b), s));
   }
   return MC_OK;
 }
@@ -219,11 +220,7 @@ MC_API int mc_dg_color_pass(mc_dg* h, int color, double* U, double* U0, double* 
   if (color < 1 || color > h->n_colors) return mc_fail(MC_EINVAL, "bad color");
   const int64_t bb = h->bounds[color - 1], e = h->bounds[color];
   if (e == bb) return MC_OK;
-  const int spw = 32 / (2 * h->ops->neq);
-  const int64_t tiles = (e - bb + spw - 1) / spw;
-  const int64_t max_blocks = (tiles + mcdg::kThreads / 32 - 1) / (mcdg::kThreads / 32);
-  int grid = h->ops->grid_colored;
-  if (grid > max_blocks) grid = int(max_blocks);
+  const int grid = colored_grid(h, e - bb);
   if (rk_mode == 0) {
     DG_TRY(h->ops->colored(h->view, U, R, nullptr, bb, e, grid, as_stream(stream)));
   } else {

@@ -9,13 +9,16 @@
 // twice in one launch, so the scatter is a plain read-modify-write:
 // no atomics, no per-surface buffer.
 //
-// Thread mapping (the "surface group"): 2*NEQ lanes per surface, lane =
-// (side, equation).  Each lane owns the N_p coefficients of ONE equation
-// of ONE element in registers, computes its own trace component, and
-// exchanges traces through warp shuffles so every lane can evaluate the
-// (nonlinear) flux; the projection onto the basis is again per lane.
-// Element blocks are [eq][j] contiguous doubles, so a lane's coefficients
-// are one contiguous run (double2 loads when N_p*8 is a multiple of 16).
+// Warp organisation ("surface group"): 2*NEQ lanes per surface, lane =
+// (side, equation).  A lane owns the N_p coefficients of ONE equation of
+// ONE element in registers: it loads them (one contiguous run, [eq][j]
+// element blocks, 16-byte vector loads), evaluates its own trace
+// components, and finally projects the fluxes back onto its basis and
+// stores.  The nonlinear flux in between needs the full state at a point,
+// so each flux is evaluated exactly ONCE per quadrature point as a warp
+// "task": traces are staged in a per-warp shared-memory scratch, the
+// warp's 32 lanes split the (surface, point) and (element, volume point)
+// tasks among themselves, and the results come back through the scratch.
 //
 // Fusion: the volume integral of an element is
 // computed in the pass where the element is first touched (its residual
@@ -33,7 +36,6 @@
 namespace mcdg {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kThreads = 256;
 
 enum Kind { TRI = 0, QUAD = 1, TET = 2 };
 enum Phys { ADV = 0, EULER = 1 };
@@ -48,9 +50,27 @@ struct Cfg {
   static constexpr int NQF = (K == TET) ? (P + 1) * (P + 1) : P + 1;
   static constexpr int NQV = (K == TET) ? (P + 1) * (P + 1) * (P + 1) : (P + 1) * (P + 1);
   static constexpr int NCODES = (K == QUAD || K == TET) ? 24 : 18;
+#ifdef MC_DG_DMMA
+  static constexpr bool DMMA_ON = (K != TET);
+#else
+  static constexpr bool DMMA_ON = false;
+#endif
   static constexpr int G = 2 * NEQ;           // lanes per surface
   static constexpr int SPW = 32 / G;          // surfaces per warp
+  static constexpr int ES = 2 * SPW;          // element slots per warp (surface kernels)
   static constexpr int GEOM = DIM + 2;        // doubles per surface geometry
+  // volume points per task chunk: about one task per lane per chunk
+  static constexpr int QC = (32 / ES) < 1 ? 1 : ((32 / ES) > NQV ? NQV : (32 / ES));
+  // block shape: tets carry large tables, use smaller blocks
+  static constexpr int WARPS = (K == TET) ? 4 : 8;
+  static constexpr int THREADS = 32 * WARPS;
+#ifndef MC_MINB_2D
+#define MC_MINB_2D 3
+#endif
+#ifndef MC_MINB_3D
+#define MC_MINB_3D 4
+#endif
+  static constexpr int MINB = (K == TET) ? MC_MINB_3D : MC_MINB_2D;
   // packed table offsets (doubles): face_phi | face_w | vol_phi | vol_dphi | vol_w
   static constexpr int T_FPHI = 0;
   static constexpr int T_FW = T_FPHI + NCODES * NQF * NP;
@@ -58,6 +78,70 @@ struct Cfg {
   static constexpr int T_VDPHI = T_VPHI + NQV * NP;
   static constexpr int T_VW = T_VDPHI + DIM * NQV * NP;
   static constexpr int T_SIZE = T_VW + NQV;
+  // shared-memory copy: rows padded to an even length so that pairs of
+  // basis values are one 16-byte broadcast load (LDS.128)
+  static constexpr int NPP = (NP + 1) & ~1;
+  static constexpr int S_FPHI = 0;
+  static constexpr int S_FW = S_FPHI + NCODES * NQF * NPP;
+  static constexpr int S_VPHI = S_FW + ((NQF + 1) & ~1);
+  static constexpr int S_VDPHI = S_VPHI + NQV * NPP;
+  static constexpr int S_VW = S_VDPHI + DIM * NQV * NPP;
+  static constexpr int S_SIZE = S_VW + ((NQV + 1) & ~1);
+  // per-warp scratch (doubles) for the surface kernels.  Every array is
+  // indexed so that the lane-parallel accesses (one lane per task or per
+  // (slot, eq)) step by an ODD number of doubles: conflict-free banks.
+  static constexpr int SV = NEQ | 1;                              // padded state stride
+  static constexpr int JIS = (DIM * DIM) | 1;                     // padded Jinv stride
+  static constexpr int W_TR = 0;                                  // [2][NQF][SPW][SV]
+  static constexpr int W_FS = W_TR + 2 * NQF * SPW * SV;          // [NQF][SPW][SV]
+  // the DMMA volume scratch {RM, VQ, FT} aliases TR/FS (used only later)
+  static constexpr int W_UNION = DMMA_ON
+      ? (8 * ((NP + 7) / 8) * 32 + 8 * 32 + 4 * DIM * 36) : 0;
+  static constexpr int W_FS_END = W_FS + NQF * SPW * SV;
+  static constexpr int W_NRM = ((W_FS_END > W_UNION ? W_FS_END : W_UNION) + 1) & ~1;  // [SPW][DIM]
+  static constexpr int W_JI = W_NRM + SPW * DIM;                  // [ES][JIS]
+  static constexpr bool VTASK = !DMMA_ON;                          // task volume path
+  static constexpr int W_VS = W_JI + ES * JIS;                    // [QC][ES][SV]
+  static constexpr int W_VF = W_VS + (VTASK ? QC * ES * SV : 0);  // [DIM][QC][ES][SV]
+  static constexpr int W_FLAG = W_VF + (VTASK ? DIM * QC * ES * SV : 0);  // ints: valid, need
+  static constexpr int W_SIZE_T = (W_FLAG + (SPW + ES + 1) / 2 + 2) & ~1;
+  // ---- FP64 tensor-core (DMMA m8n8k4) volume integral, 2D kinds -------
+  // trace  V[q][col] = sum_j Phi[q][j] C[j][col]         (MT x KT tiles)
+  // project R[j][col] = sum_kk Dt[j][kk] Ft[kk][col], kk = q*DIM + r
+  // col = element slot * NEQ + eq = lane id (32 columns = 4 N tiles)
+#ifdef MC_DG_DMMA
+  static constexpr bool DMMA = (K != TET) && (ES * NEQ == 32);
+#else
+  // measured slower than the task path on B200: fragment traffic makes the
+  // kernel shared-memory bound (profiles/)
+  static constexpr bool DMMA = false;
+#endif
+  static constexpr int MT = (NQV + 7) / 8;       // 8-point chunks / trace M tiles
+  static constexpr int KT = (NP + 3) / 4;        // trace k steps
+  static constexpr int MJ = (NP + 7) / 8;        // projection M tiles
+  static constexpr int KS = MT * 2 * DIM;        // projection k steps (4 kk rows each)
+  static constexpr int LDB = 36;                 // padded row stride of B tiles
+  static constexpr int S_AFP = S_SIZE;                     // [MT][KT][32] A fragments
+  static constexpr int S_AFD = S_AFP + MT * KT * 32;       // [MJ][KS][32]
+  static constexpr int S_TOTAL = ((DMMA ? S_AFD + MJ * KS * 32 : S_SIZE) + 1) & ~1;
+  static constexpr int D_RM = 0;                                  // [8*MJ][32]
+  static constexpr int D_VQ = D_RM + 8 * MJ * 32;                 // [8][32]
+  static constexpr int D_FT = D_VQ + 8 * 32;                      // [4*DIM][32]
+  static constexpr int D_END = D_FT + 4 * DIM * 32;
+  static constexpr int D_CM = W_SIZE_T;                           // [4*KT][LDB], persists
+  static constexpr int W_SIZE = DMMA ? (D_CM + 4 * KT * LDB) : W_SIZE_T;  // even: 16-B aligned
+  static_assert(W_SIZE % 2 == 0 && S_TOTAL % 2 == 0 && W_NRM % 2 == 0, "16-byte alignment");
+  static_assert(!DMMA || D_END <= W_NRM, "DMMA scratch must fit in the aliased region");
+  static constexpr int SMEM = (S_TOTAL + WARPS * W_SIZE) * 8;
+  // element-major volume kernel: NEQ lanes per element
+  static constexpr int EPW = 32 / NEQ;
+  static constexpr int QCV = (32 / EPW) < 1 ? 1 : ((32 / EPW) > NQV ? NQV : (32 / EPW));
+  static constexpr int V_JI = 0;
+  static constexpr int V_VS = V_JI + EPW * JIS;
+  static constexpr int V_VF = V_VS + EPW * QCV * SV;
+  static constexpr int V_FLAG = V_VF + EPW * QCV * DIM * SV;
+  static constexpr int V_SIZE = V_FLAG + (EPW + 1) / 2 + 1;
+  static constexpr int VSMEM = (S_TOTAL + WARPS * V_SIZE) * 8;
 };
 
 struct Params {
@@ -105,8 +189,7 @@ __device__ __forceinline__ void load_run(const double* __restrict__ src, double 
   }
 }
 
-// plain (non-__ldg) load for data written earlier in the same stream by
-// other launches (residual partial sums)
+// plain (coherent) load for residual partial sums written by earlier launches
 template <int N>
 __device__ __forceinline__ void load_rw(const double* src, double (&dst)[N]) {
   if constexpr ((N % 2) == 0) {
@@ -135,41 +218,62 @@ __device__ __forceinline__ void store_run(double* dst, const double (&src)[N]) {
   }
 }
 
-template <int DIM>
-__device__ __forceinline__ double sel3(int i, double a, double b, double c) {
-  return i == 0 ? a : (i == 1 ? b : c);
+// sum_j row[j] * u[j] with 16-byte loads of the (even-padded) table row
+template <int N>
+__device__ __forceinline__ double dot_row(const double* row, const double (&u)[N]) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+  double t = 0.0;
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j) {
+    const double2 a = r2[j];
+    t = fma(a.x, u[2 * j], t);
+    t = fma(a.y, u[2 * j + 1], t);
+  }
+  if constexpr (N % 2) t = fma(row[N - 1], u[N - 1], t);
+  return t;
+}
+
+// acc[j] += f * row[j]
+template <int N>
+__device__ __forceinline__ void axpy_row(const double* row, double f, double (&acc)[N]) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j) {
+    const double2 a = r2[j];
+    acc[2 * j] = fma(a.x, f, acc[2 * j]);
+    acc[2 * j + 1] = fma(a.y, f, acc[2 * j + 1]);
+  }
+  if constexpr (N % 2) acc[N - 1] = fma(row[N - 1], f, acc[N - 1]);
 }
 
 // ----------------------------------------------------------- physics
-// Normal flux component `eq` of the Lax-Friedrichs flux.  sL/sR hold the
-// full states (NEQ values) at one point; own values need no dynamic
-// indexing: the caller passes this lane's components qL = sL[eq], qR.
+// Full-state flux evaluations, one call per quadrature point (a "task").
 template <int PH, int DIM, int NEQ>
-struct Flux;
+struct Physics;
 
 template <int DIM, int NEQ>
-struct Flux<ADV, DIM, NEQ> {
-  __device__ static __forceinline__ double numerical(const double*, const double*, double qL,
-                                                     double qR, const double* n, int,
-                                                     const Params& P) {
+struct Physics<ADV, DIM, NEQ> {
+  // Fhat . n (upwind = Lax-Friedrichs with lambda = |a.n|)
+  __device__ static __forceinline__ void lf(const double* sL, const double* sR, const double* n,
+                                            const Params& P, double* out) {
     double an = P.vel[0] * n[0] + P.vel[1] * n[1];
     if (DIM == 3) an += P.vel[2] * n[2];
-    return 0.5 * an * (qL + qR) - 0.5 * fabs(an) * (qR - qL);
+    out[0] = 0.5 * an * (sL[0] + sR[0]) - 0.5 * fabs(an) * (sR[0] - sL[0]);
   }
-  // contravariant volume flux Ft_r = sum_d Jinv[r][d] F_d for own component
-  __device__ static __forceinline__ void volume(const double*, double q, const double* jinv,
-                                                int, const Params& P, double* Ft) {
+  // contravariant flux Ft[r][k] = sum_d Jinv[r][d] F_d(s)[k]
+  __device__ static __forceinline__ void vflux(const double* s, const double* ji,
+                                               const Params& P, double* Ft) {
 #pragma unroll
     for (int r = 0; r < DIM; ++r) {
-      double a = jinv[r * DIM + 0] * P.vel[0] + jinv[r * DIM + 1] * P.vel[1];
-      if (DIM == 3) a += jinv[r * DIM + 2] * P.vel[2];
-      Ft[r] = a * q;
+      double a = ji[r * DIM + 0] * P.vel[0] + ji[r * DIM + 1] * P.vel[1];
+      if (DIM == 3) a += ji[r * DIM + 2] * P.vel[2];
+      Ft[r] = a * s[0];
     }
   }
 };
 
 template <int DIM, int NEQ>
-struct Flux<EULER, DIM, NEQ> {
+struct Physics<EULER, DIM, NEQ> {
   __device__ static __forceinline__ void prim(const double* s, const Params& P, double* u,
                                               double& p) {
     const double inv = 1.0 / s[0];
@@ -182,9 +286,8 @@ struct Flux<EULER, DIM, NEQ> {
     p = (P.gamma - 1.0) * (s[NEQ - 1] - 0.5 * ke);
   }
 
-  __device__ static __forceinline__ double numerical(const double* sL, const double* sR,
-                                                     double qL, double qR, const double* n,
-                                                     int eq, const Params& P) {
+  __device__ static __forceinline__ void lf(const double* sL, const double* sR, const double* n,
+                                            const Params& P, double* out) {
     double uL[DIM], uR[DIM], pL, pR;
     prim(sL, P, uL, pL);
     prim(sR, P, uR, pR);
@@ -197,31 +300,29 @@ struct Flux<EULER, DIM, NEQ> {
     const double cL = sqrt(P.gamma * pL / sL[0]);
     const double cR = sqrt(P.gamma * pR / sR[0]);
     const double lam = fmax(fabs(vnL) + cL, fabs(vnR) + cR);
-    // F.n component: q*vn + p*m, m = 0 (mass), n_d (momentum d), vn (energy)
-    double nm = 0.0;
-    if (eq >= 1 && eq <= DIM) nm = sel3<DIM>(eq - 1, n[0], n[1], DIM == 3 ? n[2] : 0.0);
-    const bool energy = eq == NEQ - 1;
-    const double fL = qL * vnL + pL * (energy ? vnL : nm);
-    const double fR = qR * vnR + pR * (energy ? vnR : nm);
-    return 0.5 * (fL + fR) - 0.5 * lam * (qR - qL);
+    // F.n = s*vn + p*(0, n, vn)
+    out[0] = 0.5 * (sL[0] * vnL + sR[0] * vnR) - 0.5 * lam * (sR[0] - sL[0]);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+      out[1 + d] = 0.5 * ((sL[1 + d] * vnL + pL * n[d]) + (sR[1 + d] * vnR + pR * n[d])) -
+                   0.5 * lam * (sR[1 + d] - sL[1 + d]);
+    out[NEQ - 1] = 0.5 * ((sL[NEQ - 1] + pL) * vnL + (sR[NEQ - 1] + pR) * vnR) -
+                   0.5 * lam * (sR[NEQ - 1] - sL[NEQ - 1]);
   }
 
-  __device__ static __forceinline__ void volume(const double* s, double q, const double* jinv,
-                                                int eq, const Params& P, double* Ft) {
+  __device__ static __forceinline__ void vflux(const double* s, const double* ji,
+                                               const Params& P, double* Ft) {
     double u[DIM], p;
     prim(s, P, u, p);
-    const bool energy = eq == NEQ - 1;
-    const double coef = energy ? q + p : q;
 #pragma unroll
     for (int r = 0; r < DIM; ++r) {
       double ut = 0.0;
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) ut += jinv[r * DIM + d] * u[d];
-      double extra = 0.0;
-      if (eq >= 1 && eq <= DIM)
-        extra = p * sel3<DIM>(eq - 1, jinv[r * DIM + 0], jinv[r * DIM + 1],
-                              DIM == 3 ? jinv[r * DIM + 2] : 0.0);
-      Ft[r] = coef * ut + extra;
+      for (int d = 0; d < DIM; ++d) ut += ji[r * DIM + d] * u[d];
+      Ft[r * NEQ + 0] = s[0] * ut;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) Ft[r * NEQ + 1 + d] = s[1 + d] * ut + p * ji[r * DIM + d];
+      Ft[r * NEQ + NEQ - 1] = (s[NEQ - 1] + p) * ut;
     }
   }
 };
@@ -229,83 +330,199 @@ struct Flux<EULER, DIM, NEQ> {
 // ------------------------------------------------- table staging (smem)
 template <class C>
 __device__ __forceinline__ void stage_tables(const double* __restrict__ g, double* s) {
-  for (int i = threadIdx.x; i < C::T_SIZE; i += blockDim.x) s[i] = __ldg(g + i);
+  // compact global layout -> padded shared layout
+  for (int i = threadIdx.x; i < C::S_SIZE; i += blockDim.x) {
+    double v = 0.0;
+    if (i < C::S_FW) {
+      const int row = i / C::NPP, j = i - row * C::NPP;
+      if (j < C::NP) v = __ldg(g + C::T_FPHI + row * C::NP + j);
+    } else if (i < C::S_VPHI) {
+      const int k = i - C::S_FW;
+      if (k < C::NQF) v = __ldg(g + C::T_FW + k);
+    } else if (i < C::S_VW) {
+      const int row = (i - C::S_VPHI) / C::NPP, j = (i - C::S_VPHI) - row * C::NPP;
+      if (j < C::NP) v = __ldg(g + C::T_VPHI + row * C::NP + j);  // vphi and vdphi rows
+    } else {
+      const int k = i - C::S_VW;
+      if (k < C::NQV) v = __ldg(g + C::T_VW + k);
+    }
+    s[i] = v;
+  }
+  if constexpr (C::DMMA) {
+    __syncthreads();
+    // A fragments (row = lane >> 2, k = lane & 3) of Phi and of Dt
+    for (int i = threadIdx.x; i < C::MT * C::KT * 32; i += blockDim.x) {
+      const int l = i & 31, mk = i >> 5, m = mk / C::KT, k = mk - m * C::KT;
+      const int q = 8 * m + (l >> 2), j = 4 * k + (l & 3);
+      s[C::S_AFP + i] = (q < C::NQV && j < C::NP) ? s[C::S_VPHI + q * C::NPP + j] : 0.0;
+    }
+    for (int i = threadIdx.x; i < C::MJ * C::KS * 32; i += blockDim.x) {
+      const int l = i & 31, mk = i >> 5, mj = mk / C::KS, kst = mk - mj * C::KS;
+      // k step kst covers dimension r = kst % DIM of the 4 points 4*(kst / DIM) + 0..3
+      const int j = 8 * mj + (l >> 2), r = kst % C::DIM, q = 4 * (kst / C::DIM) + (l & 3);
+      s[C::S_AFD + i] = (j < C::NP && q < C::NQV) ? s[C::S_VDPHI + (r * C::NQV + q) * C::NPP + j] : 0.0;
+    }
+  }
   __syncthreads();
 }
 
-// Volume contribution of one element for this lane's equation, added into
-// acc.  All lanes of the warp must call it (shuffles); `base` is the first
-// lane of this lane's element group (NEQ lanes).
-template <class C, int PH>
-__device__ __forceinline__ void volume_into(const double* st, const double (&u)[C::NP],
-                                            const double* jinv, int base, int eq,
-                                            const Params& prm, double (&acc)[C::NP]) {
-  const double* vphi = st + C::T_VPHI;
-  const double* vdphi = st + C::T_VDPHI;
-  const double* vw = st + C::T_VW;
+// Volume integral of the warp's NS element slots, added into acc of the
+// lanes whose slot needs it.  Warp-uniform control flow; `vs`, `vf`, `ji`,
+// `need` live in the warp scratch; slot jinv/need were written earlier.
+// Task t = (point qq, slot e) with e fastest, so task-parallel scratch
+// accesses step by the odd stride SV (bank-conflict free).
+template <class C, int PH, int NS, int QCH>
+__device__ __forceinline__ void volume_tasks(const double* st, double* vs, double* vf,
+                                             const double* ji, const int* need,
+                                             const double (&u)[C::NP], int slot, int eq,
+                                             bool mine, int lane, const Params& prm,
+                                             double (&acc)[C::NP]) {
+  const double* vphi = st + C::S_VPHI;
+  const double* vdphi = st + C::S_VDPHI;
+  const double* vw = st + C::S_VW;
 #pragma unroll 1
-  for (int q = 0; q < C::NQV; ++q) {
-    double uq = 0.0;
-#pragma unroll
-    for (int j = 0; j < C::NP; ++j) uq = fma(vphi[q * C::NP + j], u[j], uq);
-    double s[C::NEQ];
-#pragma unroll
-    for (int k = 0; k < C::NEQ; ++k) s[k] = __shfl_sync(kFull, uq, base + k);
-    double Ft[C::DIM];
-    Flux<PH, C::DIM, C::NEQ>::volume(s, uq, jinv, eq, prm, Ft);
-    const double w = vw[q];
-#pragma unroll
-    for (int r = 0; r < C::DIM; ++r) Ft[r] *= w;
-#pragma unroll
-    for (int j = 0; j < C::NP; ++j) {
-      double t = acc[j];
-#pragma unroll
-      for (int r = 0; r < C::DIM; ++r) t = fma(vdphi[(r * C::NQV + q) * C::NP + j], Ft[r], t);
-      acc[j] = t;
+  for (int q0 = 0; q0 < C::NQV; q0 += QCH) {
+    const int nq = (C::NQV - q0) < QCH ? (C::NQV - q0) : QCH;
+    if (mine) {
+      for (int qq = 0; qq < nq; ++qq)
+        vs[(qq * NS + slot) * C::SV + eq] = dot_row<C::NP>(vphi + (q0 + qq) * C::NPP, u);
     }
+    __syncwarp();
+    for (int t = lane; t < NS * QCH; t += 32) {
+      const int qq = t / NS, e = t - qq * NS;
+      if (qq < nq && need[e]) {
+        double s[C::NEQ], Ft[C::DIM * C::NEQ];
+#pragma unroll
+        for (int k = 0; k < C::NEQ; ++k) s[k] = vs[t * C::SV + k];
+        Physics<PH, C::DIM, C::NEQ>::vflux(s, ji + e * C::JIS, prm, Ft);
+        const double w = vw[q0 + qq];
+#pragma unroll
+        for (int r = 0; r < C::DIM; ++r) {
+#pragma unroll
+          for (int k = 0; k < C::NEQ; ++k)
+            vf[(r * QCH * NS + t) * C::SV + k] = w * Ft[r * C::NEQ + k];
+        }
+      }
+    }
+    __syncwarp();
+    if (mine) {
+      for (int qq = 0; qq < nq; ++qq) {
+#pragma unroll
+        for (int r = 0; r < C::DIM; ++r) {
+          const double f = vf[((r * QCH + qq) * NS + slot) * C::SV + eq];
+          axpy_row<C::NP>(vdphi + (r * C::NQV + q0 + qq) * C::NPP, f, acc);
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
-// Surface contribution of one surface for this lane (side, eq) into acc.
+// D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor core.  Fragments:
+// a = A[lane>>2][lane&3], b = B[lane&3][lane>>2], (d0,d1) = D[lane>>2][2(lane&3)+{0,1}]
+__device__ __forceinline__ void dmma(double a, double b, double& d0, double& d1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// Volume integral through DMMA (all 32 lanes = 32 (slot, eq) columns).
+// Per 8-point chunk: trace (DMMA) -> VQ; per half chunk of 4 points one
+// flux task per (point, slot) -> FT; projection (DMMA) accumulates in RM.
+// VQ / FT / RM rows are XOR-swizzled so that both the fragment accesses and
+// the task accesses hit each bank pair at most twice (2 wavefronts).
+__device__ __forceinline__ int swz8(int row) { return (row & 3) | ((row & 4) << 1); }
+__device__ __forceinline__ int swzf(int row) {  // FT rows: (0, 1, 10, 11)[row & 3]
+  return (row & 1) | ((row & 2) ? 10 : 0);
+}
+
 template <class C, int PH>
-__device__ __forceinline__ void surface_into(const double* st, const double (&u)[C::NP],
-                                             bool has, bool boundary, int mycode, int side,
-                                             int eq, int lane, int grp_base, const double* n,
-                                             double scale, const Params& prm,
-                                             double (&acc)[C::NP]) {
-  const double* fphi = st + C::T_FPHI + mycode * (C::NQF * C::NP);
-  const double* fw = st + C::T_FW;
-  const double sign = side ? 1.0 : -1.0;
+__device__ __forceinline__ void volume_dmma(const double* st, double* ws, const int* need,
+                                            const double (&u)[C::NP], bool mine, int lane,
+                                            const Params& prm, double (&acc)[C::NP]) {
+  double* cm = ws + C::D_CM;
+  double* rm = ws + C::D_RM;
+  double* vq = ws + C::D_VQ;
+  double* ft = ws + C::D_FT;
+  const double* ji = ws + C::W_JI;
+  const double* afp = st + C::S_AFP;
+  const double* afd = st + C::S_AFD;
+  const double* vw = st + C::S_VW;
+  const int r4 = lane & 3, c8 = lane >> 2;
+#pragma unroll
+  for (int j = 0; j < C::NP; ++j) cm[j * C::LDB + lane] = u[j];
+  __syncwarp();
 #pragma unroll 1
-  for (int g = 0; g < C::NQF; ++g) {
-    double tr = 0.0;
-    if (has) {
+  for (int m = 0; m < C::MT; ++m) {
 #pragma unroll
-      for (int j = 0; j < C::NP; ++j) tr = fma(fphi[g * C::NP + j], u[j], tr);
+    for (int n = 0; n < 4; ++n) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < C::KT; ++k)
+        dmma(afp[(m * C::KT + k) * 32 + lane], cm[(4 * k + r4) * C::LDB + 8 * n + c8], d0, d1);
+      const int col = 8 * n + 2 * r4, g = swz8(c8);
+      vq[c8 * 32 + (col ^ g)] = d0;
+      vq[c8 * 32 + ((col + 1) ^ g)] = d1;
     }
-    double sL[C::NEQ], sR[C::NEQ];
+    __syncwarp();
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      if (8 * m + 4 * h >= C::NQV) break;           // warp-uniform
+      for (int t = lane; t < 4 * C::ES; t += 32) {
+        const int qq = t / C::ES, e = t - qq * C::ES;
+        const int q = 8 * m + 4 * h + qq;
+        double Ft[C::DIM * C::NEQ];
+        if (q < C::NQV && need[e]) {
+          double sv[C::NEQ];
+          const int row = 4 * h + qq, g = swz8(row);
 #pragma unroll
-    for (int k = 0; k < C::NEQ; ++k) {
-      sL[k] = __shfl_sync(kFull, tr, grp_base + k);
-      sR[k] = __shfl_sync(kFull, tr, grp_base + C::NEQ + k);
+          for (int k = 0; k < C::NEQ; ++k) sv[k] = vq[row * 32 + ((e * C::NEQ + k) ^ g)];
+          Physics<PH, C::DIM, C::NEQ>::vflux(sv, ji + e * C::JIS, prm, Ft);
+          const double w = vw[q];
+#pragma unroll
+          for (int k = 0; k < C::DIM * C::NEQ; ++k) Ft[k] *= w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < C::DIM * C::NEQ; ++k) Ft[k] = 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < C::DIM; ++r) {
+          const int row = 4 * r + qq, g = swzf(row);
+#pragma unroll
+          for (int k = 0; k < C::NEQ; ++k) ft[row * 32 + ((e * C::NEQ + k) ^ g)] = Ft[r * C::NEQ + k];
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mj = 0; mj < C::MJ; ++mj) {
+        const int row = 8 * mj + c8, g = swz8(c8);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          const int col = 8 * n + 2 * r4;
+          double c0 = 0.0, c1 = 0.0;
+          if (m > 0 || h > 0) {
+            c0 = rm[row * 32 + (col ^ g)];
+            c1 = rm[row * 32 + ((col + 1) ^ g)];
+          }
+#pragma unroll
+          for (int sl = 0; sl < C::DIM; ++sl)
+            dmma(afd[(mj * C::KS + (2 * m + h) * C::DIM + sl) * 32 + lane],
+                 ft[(4 * sl + r4) * 32 + ((8 * n + c8) ^ swzf(r4))], c0, c1);
+          rm[row * 32 + (col ^ g)] = c0;
+          rm[row * 32 + ((col + 1) ^ g)] = c1;
+        }
+      }
+      __syncwarp();
     }
-    // partner value of this lane's own equation
-    double qL = __shfl_sync(kFull, tr, grp_base + eq);
-    double qR = __shfl_sync(kFull, tr, grp_base + C::NEQ + eq);
-    if (boundary) {  // far-field ghost state
-#pragma unroll
-      for (int k = 0; k < C::NEQ; ++k) sR[k] = prm.ff[k];
-      qR = prm.ff[eq];
-    }
-    const double fh = Flux<PH, C::DIM, C::NEQ>::numerical(sL, sR, qL, qR, n, eq, prm);
-    const double coef = sign * scale * fw[g] * fh;
-#pragma unroll
-    for (int j = 0; j < C::NP; ++j) acc[j] = fma(coef, fphi[g * C::NP + j], acc[j]);
   }
+  if (mine) {
+#pragma unroll
+    for (int j = 0; j < C::NP; ++j) acc[j] += rm[j * 32 + (lane ^ swz8(j & 7))];
+  }
+  __syncwarp();
 }
 
 struct Lane {
-  int lane, grp, r, side, eq, grp_base, side_base;
+  int lane, grp, side, eq, slot;
   bool active;
 };
 
@@ -314,83 +531,161 @@ __device__ __forceinline__ Lane lane_info() {
   Lane L;
   L.lane = threadIdx.x & 31;
   L.grp = L.lane / C::G;
-  L.r = L.lane - L.grp * C::G;
-  L.side = L.r / C::NEQ;
-  L.eq = L.r - L.side * C::NEQ;
+  const int r = L.lane - L.grp * C::G;
+  L.side = r / C::NEQ;
+  L.eq = r - L.side * C::NEQ;
   L.active = L.grp < C::SPW;
-  if (!L.active) {  // idle tail lanes shadow group 0 (results discarded)
-    L.grp = 0;
-  }
-  L.grp_base = L.grp * C::G;
-  L.side_base = L.grp_base + L.side * C::NEQ;
+  if (!L.active) L.grp = 0;   // idle tail lanes never write shared state
+  L.slot = 2 * L.grp + L.side;
   return L;
+}
+
+// Per-surface part shared by the colored and uncolored kernels: metadata,
+// traces into the scratch, one LF flux per (surface, point) task, and the
+// lift of this lane's flux component into acc.
+struct SurfCtx {
+  int L, R, e, mycode;
+  uint32_t code;
+  double scale;
+  bool valid, has, owner, boundary;
+};
+
+template <class C>
+__device__ __forceinline__ SurfCtx load_surface(const View& v, const Lane& ln, int64_t s,
+                                                int64_t end, double* ws) {
+  SurfCtx c;
+  c.valid = ln.active && s < end;
+  c.L = 0;
+  c.R = -1;
+  c.code = 0;
+  c.scale = 0.0;
+  if (c.valid) {
+    c.L = __ldg(v.left + s);
+    c.R = __ldg(v.right + s);
+    c.code = __ldg(v.code + s);
+    const double* gm = v.geom + s * C::GEOM;
+    c.scale = __ldg(gm + C::DIM + ln.side);
+    if (ln.side == 0 && ln.eq == 0) {
+#pragma unroll
+      for (int d = 0; d < C::DIM; ++d) ws[C::W_NRM + ln.grp * C::DIM + d] = __ldg(gm + d);
+    }
+  }
+  c.boundary = c.R < 0;
+  c.e = ln.side ? c.R : c.L;
+  c.has = c.valid && c.e >= 0;
+  c.owner = c.has && !(ln.side && (c.code & MC_FLAG_R_GHOST));
+  c.mycode = ln.side ? int((c.code >> 6) & 63u) : int(c.code & 63u);
+  return c;
+}
+
+template <class C, int PH>
+__device__ __forceinline__ void surface_tasks(const double* st, double* ws, const Lane& ln,
+                                              const SurfCtx& c, const double (&u)[C::NP],
+                                              const Params& prm, double (&acc)[C::NP]) {
+  const double* fphi = st + C::S_FPHI + c.mycode * (C::NQF * C::NPP);
+  const double* fw = st + C::S_FW;
+  int* valid = reinterpret_cast<int*>(ws + C::W_FLAG);
+  if (ln.active && ln.side == 0 && ln.eq == 0) valid[ln.grp] = c.valid;
+  if (ln.active) {
+#pragma unroll 1
+    for (int g = 0; g < C::NQF; ++g) {
+      double tr = 0.0;
+      if (c.has) {
+#pragma unroll
+        tr = dot_row<C::NP>(fphi + g * C::NPP, u);
+      } else if (c.valid && ln.side == 1) {
+        tr = prm.ff[ln.eq];  // far-field ghost state on physical boundaries
+      }
+      ws[C::W_TR + ((ln.side * C::NQF + g) * C::SPW + ln.grp) * C::SV + ln.eq] = tr;
+    }
+  }
+  __syncwarp();
+  for (int t = ln.lane; t < C::SPW * C::NQF; t += 32) {
+    const int g = t / C::SPW, gs = t - g * C::SPW;
+    if (valid[gs]) {
+      double sL[C::NEQ], sR[C::NEQ], n[C::DIM], out[C::NEQ];
+#pragma unroll
+      for (int k = 0; k < C::NEQ; ++k) {
+        sL[k] = ws[C::W_TR + t * C::SV + k];
+        sR[k] = ws[C::W_TR + (C::NQF * C::SPW + t) * C::SV + k];
+      }
+#pragma unroll
+      for (int d = 0; d < C::DIM; ++d) n[d] = ws[C::W_NRM + gs * C::DIM + d];
+      Physics<PH, C::DIM, C::NEQ>::lf(sL, sR, n, prm, out);
+      const double w = fw[g];
+#pragma unroll
+      for (int k = 0; k < C::NEQ; ++k) ws[C::W_FS + t * C::SV + k] = w * out[k];
+    }
+  }
+  __syncwarp();
+  if (c.owner) {
+    const double sc = ln.side ? c.scale : -c.scale;
+#pragma unroll 1
+    for (int g = 0; g < C::NQF; ++g) {
+      const double f = sc * ws[C::W_FS + (g * C::SPW + ln.grp) * C::SV + ln.eq];
+      axpy_row<C::NP>(fphi + g * C::NPP, f, acc);
+    }
+  }
+  __syncwarp();
 }
 
 // --------------------------------------------------------------- kernels
 // One color: surfaces [begin, end) of the color-major list.
 template <class C, int PH, bool kRK>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
 k_surface_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
                   int64_t end) {
-  extern __shared__ double st[];
+  extern __shared__ double sm[];
+  double* st = sm;
   stage_tables<C>(v.tables, st);
   const Lane ln = lane_info<C>();
+  double* ws = sm + C::S_TOTAL + (threadIdx.x >> 5) * C::W_SIZE;
+  int* need = reinterpret_cast<int*>(ws + C::W_FLAG) + C::SPW;
+  if constexpr (C::DMMA) {  // CM rows beyond N_p stay zero (B padding of the trace)
+    for (int i = ln.lane; i < (4 * C::KT - C::NP) * C::LDB; i += 32)
+      ws[C::D_CM + C::NP * C::LDB + i] = 0.0;
+    __syncwarp();
+  }
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t tile = begin + warp * C::SPW; tile < end; tile += nwarp * C::SPW) {
     const int64_t s = tile + ln.grp;
-    const bool valid = ln.active && s < end;
-    int L = 0, Rr = -1;
-    uint32_t code = 0;
-    double n[C::DIM];
-    double scale = 0.0;
-    if (s < end) {
-      L = __ldg(v.left + s);
-      Rr = __ldg(v.right + s);
-      code = __ldg(v.code + s);
-      const double* gm = v.geom + s * C::GEOM;
-#pragma unroll
-      for (int d = 0; d < C::DIM; ++d) n[d] = __ldg(gm + d);
-      scale = __ldg(gm + C::DIM + ln.side);
-    } else {
-#pragma unroll
-      for (int d = 0; d < C::DIM; ++d) n[d] = 0.0;
-      n[0] = 1.0;
-    }
-    const bool boundary = Rr < 0;
-    const int e = ln.side ? Rr : L;
-    const bool ghost = ln.side && (code & MC_FLAG_R_GHOST);
-    const bool has = valid && e >= 0;
-    const bool owner = has && !ghost;
-    const int mycode = ln.side ? int((code >> 6) & 63u) : int(code & 63u);
-    const bool first = owner && (code & (ln.side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
-    const bool last = owner && (code & (ln.side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
-
+    const SurfCtx c = load_surface<C>(v, ln, s, end, ws);
+    const bool first = c.owner && (c.code & (ln.side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
+    const bool last = c.owner && (c.code & (ln.side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
+    const int64_t off = int64_t(c.has ? c.e : 0) * v.stride + ln.eq * C::NP;
     double u[C::NP], acc[C::NP];
-    const int64_t off = int64_t(has ? e : 0) * v.stride + ln.eq * C::NP;
-    if (has) {
+    if (c.has) {
       load_run<C::NP>(U + off, u);
     } else {
 #pragma unroll
       for (int j = 0; j < C::NP; ++j) u[j] = 0.0;
     }
+    if (c.owner && !first) {
+      load_rw<C::NP>(R + off, acc);
+    } else {
 #pragma unroll
-    for (int j = 0; j < C::NP; ++j) acc[j] = 0.0;
-    if (__any_sync(kFull, first)) {
-      double jinv[C::DIM * C::DIM];
-      const double* jp = v.jinv + int64_t(has ? e : 0) * (C::DIM * C::DIM);
-#pragma unroll
-      for (int k = 0; k < C::DIM * C::DIM; ++k) jinv[k] = has ? __ldg(jp + k) : 0.0;
-      volume_into<C, PH>(st, u, jinv, ln.side_base, ln.eq, v.prm, acc);
-      if (!first) {
-#pragma unroll
-        for (int j = 0; j < C::NP; ++j) acc[j] = 0.0;
-      }
+      for (int j = 0; j < C::NP; ++j) acc[j] = 0.0;
     }
-    if (owner && !first) load_rw<C::NP>(R + off, acc);
-    surface_into<C, PH>(st, u, has, boundary, mycode, ln.side, ln.eq, ln.lane, ln.grp_base, n,
-                        scale, v.prm, acc);
-    if (owner) {
+    if (__any_sync(kFull, first)) {
+      if (ln.active && ln.eq == 0) {
+        need[ln.slot] = first;
+        if (first) {
+          const double* jp = v.jinv + int64_t(c.e) * (C::DIM * C::DIM);
+#pragma unroll
+          for (int k = 0; k < C::DIM * C::DIM; ++k)
+            ws[C::W_JI + ln.slot * C::JIS + k] = __ldg(jp + k);
+        }
+      }
+      __syncwarp();
+      if constexpr (C::DMMA)
+        volume_dmma<C, PH>(st, ws, need, u, first && ln.active, ln.lane, v.prm, acc);
+      else
+        volume_tasks<C, PH, C::ES, C::QC>(st, ws + C::W_VS, ws + C::W_VF, ws + C::W_JI, need, u,
+                                          ln.slot, ln.eq, first && ln.active, ln.lane, v.prm, acc);
+    }
+    surface_tasks<C, PH>(st, ws, ln, c, u, v.prm, acc);
+    if (c.owner) {
       if (kRK && last) {
         if (rk.save_u0) store_run<C::NP>(rk.U0 + off, u);
         if (rk.a != 0.0) {
@@ -410,37 +705,47 @@ k_surface_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk,
   }
 }
 
-// Volume integral for all owned elements: NEQ lanes per element.
+// Volume integral for all owned elements (buffered / atomic strategies):
+// NEQ lanes per element, same task scheme.
 template <class C, int PH>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
 k_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
-  extern __shared__ double st[];
+  extern __shared__ double sm[];
+  double* st = sm;
   stage_tables<C>(v.tables, st);
-  constexpr int EPW = 32 / C::NEQ;
+  double* ws = sm + C::S_TOTAL + (threadIdx.x >> 5) * C::V_SIZE;
+  int* need = reinterpret_cast<int*>(ws + C::V_FLAG);
   const int lane = threadIdx.x & 31;
-  int grp = lane / C::NEQ;
-  const int eq = lane - grp * C::NEQ;
-  const bool act = grp < EPW;
-  if (!act) grp = 0;
-  const int base = grp * C::NEQ;
+  int slot = lane / C::NEQ;
+  const int eq = lane - slot * C::NEQ;
+  const bool act = slot < C::EPW;
+  if (!act) slot = 0;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t tile = warp * EPW; tile < v.n_elements; tile += nwarp * EPW) {
-    const int64_t e = tile + grp;
+  for (int64_t tile = warp * C::EPW; tile < v.n_elements; tile += nwarp * C::EPW) {
+    const int64_t e = tile + slot;
     const bool has = act && e < v.n_elements;
     const int64_t off = (has ? e : 0) * v.stride + eq * C::NP;
-    double u[C::NP], acc[C::NP], jinv[C::DIM * C::DIM];
-    if (has) load_run<C::NP>(U + off, u);
-    else {
+    double u[C::NP], acc[C::NP];
+    if (has) {
+      load_run<C::NP>(U + off, u);
+    } else {
 #pragma unroll
       for (int j = 0; j < C::NP; ++j) u[j] = 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < C::DIM * C::DIM; ++k)
-      jinv[k] = has ? __ldg(v.jinv + (has ? e : 0) * (C::DIM * C::DIM) + k) : 0.0;
-#pragma unroll
     for (int j = 0; j < C::NP; ++j) acc[j] = 0.0;
-    volume_into<C, PH>(st, u, jinv, base, eq, v.prm, acc);
+    if (act && eq == 0) {
+      need[slot] = has;
+      if (has) {
+#pragma unroll
+        for (int k = 0; k < C::DIM * C::DIM; ++k)
+          ws[C::V_JI + slot * C::JIS + k] = __ldg(v.jinv + e * (C::DIM * C::DIM) + k);
+      }
+    }
+    __syncwarp();
+    volume_tasks<C, PH, C::EPW, C::QCV>(st, ws + C::V_VS, ws + C::V_VF, ws + C::V_JI, need, u,
+                                        slot, eq, has, lane, v.prm, acc);
     if (has) store_run<C::NP>(R + off, acc);
   }
 }
@@ -448,60 +753,39 @@ k_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
 // Surface contributions of ALL surfaces (no coloring) to either the
 // 2*ns buffer (kAtomic = false: slot 2s+side) or atomically into R.
 template <class C, int PH, bool kAtomic>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
 k_surface_uncolored(View v, const double* __restrict__ U, double* __restrict__ out) {
-  extern __shared__ double st[];
+  extern __shared__ double sm[];
+  double* st = sm;
   stage_tables<C>(v.tables, st);
   const Lane ln = lane_info<C>();
+  double* ws = sm + C::S_TOTAL + (threadIdx.x >> 5) * C::W_SIZE;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t end = v.n_surfaces;
   for (int64_t tile = warp * C::SPW; tile < end; tile += nwarp * C::SPW) {
     const int64_t s = tile + ln.grp;
-    const bool valid = ln.active && s < end;
-    int L = 0, Rr = -1;
-    uint32_t code = 0;
-    double n[C::DIM];
-    double scale = 0.0;
-    if (s < end) {
-      L = __ldg(v.left + s);
-      Rr = __ldg(v.right + s);
-      code = __ldg(v.code + s);
-      const double* gm = v.geom + s * C::GEOM;
-#pragma unroll
-      for (int d = 0; d < C::DIM; ++d) n[d] = __ldg(gm + d);
-      scale = __ldg(gm + C::DIM + ln.side);
-    } else {
-#pragma unroll
-      for (int d = 0; d < C::DIM; ++d) n[d] = 0.0;
-      n[0] = 1.0;
-    }
-    const bool boundary = Rr < 0;
-    const int e = ln.side ? Rr : L;
-    const bool ghost = ln.side && (code & MC_FLAG_R_GHOST);
-    const bool has = valid && e >= 0;
-    const bool owner = has && !ghost;
-    const int mycode = ln.side ? int((code >> 6) & 63u) : int(code & 63u);
+    const SurfCtx c = load_surface<C>(v, ln, s, end, ws);
     double u[C::NP], acc[C::NP];
-    if (has) load_run<C::NP>(U + int64_t(e) * v.stride + ln.eq * C::NP, u);
-    else {
+    if (c.has) {
+      load_run<C::NP>(U + int64_t(c.e) * v.stride + ln.eq * C::NP, u);
+    } else {
 #pragma unroll
       for (int j = 0; j < C::NP; ++j) u[j] = 0.0;
     }
 #pragma unroll
     for (int j = 0; j < C::NP; ++j) acc[j] = 0.0;
-    surface_into<C, PH>(st, u, has, boundary, mycode, ln.side, ln.eq, ln.lane, ln.grp_base, n,
-                        scale, v.prm, acc);
+    surface_tasks<C, PH>(st, ws, ln, c, u, v.prm, acc);
     if (kAtomic) {
-      if (owner) {
-        double* dst = out + int64_t(e) * v.stride + ln.eq * C::NP;
+      if (c.owner) {
+        double* dst = out + int64_t(c.e) * v.stride + ln.eq * C::NP;
 #pragma unroll
         for (int j = 0; j < C::NP; ++j) atomicAdd(dst + j, acc[j]);
       }
-    } else if (valid) {
+    } else if (c.valid) {
       // buffer slot 2s+side holds this side's contribution (0 if absent)
       double* dst = out + (2 * s + ln.side) * v.stride + ln.eq * C::NP;
-      if (!owner) {
+      if (!c.owner) {
 #pragma unroll
         for (int j = 0; j < C::NP; ++j) acc[j] = 0.0;
       }
@@ -509,6 +793,8 @@ k_surface_uncolored(View v, const double* __restrict__ U, double* __restrict__ o
     }
   }
 }
+
+constexpr int kThreads = 256;
 
 // Buffer-and-reduce phase two: R[e] += sum of its slots (local side order).
 template <class C>
@@ -525,15 +811,6 @@ k_gather(View v, const double* __restrict__ buf, double* __restrict__ R) {
     for (int64_t t = b; t < f; ++t) acc += __ldg(buf + int64_t(__ldg(v.slots + t)) * v.stride + k);
     R[e * v.stride + k] = acc;
   }
-}
-
-// U <- a*U0 + b*(U + dt*R) over owned blocks (unfused strategies).
-static __global__ void __launch_bounds__(kThreads)
-k_rk_update(int64_t n, double* __restrict__ U, const double* __restrict__ U0,
-            const double* __restrict__ R, double a, double b, double dt) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    U[i] = a * U0[i] + b * fma(dt, R[i], U[i]);
 }
 
 }  // namespace mcdg

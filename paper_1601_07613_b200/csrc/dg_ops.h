@@ -4,12 +4,14 @@
 #include <stdint.h>
 
 #include "dg_kernels.cuh"
+#include "dg_tpe.cuh"
 
 namespace mcdg {
 
 struct Ops {
   int dim, neq, np, nqf, nqv, ncodes, table_size;
-  int smem_bytes;
+  int threads;                                     // block size of the task kernels
+  int spw;                                         // surfaces per warp
   int grid_colored, grid_volume, grid_uncolored;   // resident-grid sizes
   cudaError_t (*colored)(const View&, double* U, double* R, const RK* rk, int64_t b,
                          int64_t e, int grid, cudaStream_t s);
@@ -25,34 +27,47 @@ Ops* ops_tri(int phys, int p);
 Ops* ops_quad(int phys, int p);
 Ops* ops_tet(int phys, int p);
 
-cudaError_t rk_update(int64_t n, double* U, const double* U0, const double* R, double a,
-                      double b, double dt, cudaStream_t s);
-
 // Instantiation helper used by the per-kind translation units.
 template <int K, int PH, int P>
 struct Instance {
   using C = Cfg<K, PH, P>;
+  using T = Tpe<C>;
   static cudaError_t colored(const View& v, double* U, double* R, const RK* rk, int64_t b,
                              int64_t e, int grid, cudaStream_t s) {
-    const int smem = C::T_SIZE * int(sizeof(double));
-    if (rk)
-      k_surface_colored<C, PH, true><<<grid, kThreads, smem, s>>>(v, U, R, *rk, b, e);
-    else
-      k_surface_colored<C, PH, false><<<grid, kThreads, smem, s>>>(v, U, R, RK{}, b, e);
+    if constexpr (T::OK) {
+      if (rk)
+        k_tpe_colored<C, PH, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, *rk, b, e);
+      else
+        k_tpe_colored<C, PH, false><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, RK{}, b, e);
+    } else {
+      if (rk)
+        k_surface_colored<C, PH, true><<<grid, C::THREADS, C::SMEM, s>>>(v, U, R, *rk, b, e);
+      else
+        k_surface_colored<C, PH, false><<<grid, C::THREADS, C::SMEM, s>>>(v, U, R, RK{}, b, e);
+    }
     return cudaGetLastError();
   }
   static cudaError_t volume(const View& v, const double* U, double* R, int grid,
                             cudaStream_t s) {
-    k_volume<C, PH><<<grid, kThreads, C::T_SIZE * int(sizeof(double)), s>>>(v, U, R);
+    if constexpr (T::OK)
+      k_tpe_volume<C, PH><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R);
+    else
+      k_volume<C, PH><<<grid, C::THREADS, C::VSMEM, s>>>(v, U, R);
     return cudaGetLastError();
   }
   static cudaError_t uncolored(const View& v, const double* U, double* out, bool atomic,
                                int grid, cudaStream_t s) {
-    const int smem = C::T_SIZE * int(sizeof(double));
-    if (atomic)
-      k_surface_uncolored<C, PH, true><<<grid, kThreads, smem, s>>>(v, U, out);
-    else
-      k_surface_uncolored<C, PH, false><<<grid, kThreads, smem, s>>>(v, U, out);
+    if constexpr (T::OK) {
+      if (atomic)
+        k_tpe_uncolored<C, PH, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, out);
+      else
+        k_tpe_uncolored<C, PH, false><<<grid, T::THREADS, T::SMEM, s>>>(v, U, out);
+    } else {
+      if (atomic)
+        k_surface_uncolored<C, PH, true><<<grid, C::THREADS, C::SMEM, s>>>(v, U, out);
+      else
+        k_surface_uncolored<C, PH, false><<<grid, C::THREADS, C::SMEM, s>>>(v, U, out);
+    }
     return cudaGetLastError();
   }
   static cudaError_t gather(const View& v, const double* buf, double* R, cudaStream_t s) {
@@ -64,33 +79,42 @@ struct Instance {
     return cudaGetLastError();
   }
   static cudaError_t init(Ops* o) {
-    const int smem = C::T_SIZE * int(sizeof(double));
     int dev = 0, sms = 148, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t err;
-    auto fit = [&](const void* fn, int* grid) -> cudaError_t {
+    auto fit = [&](const void* fn, int smem, int threads, int* grid) -> cudaError_t {
       cudaError_t e2 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e2 != cudaSuccess) return e2;
-      e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem);
+      e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
       if (e2 != cudaSuccess) return e2;
       *grid = sms * (occ > 0 ? occ : 1);
       return cudaSuccess;
     };
-    if ((err = fit((const void*)k_surface_colored<C, PH, true>, &o->grid_colored))) return err;
+    cudaError_t err;
     int g2 = 0;
-    if ((err = fit((const void*)k_surface_colored<C, PH, false>, &g2))) return err;
-    if (g2 < o->grid_colored) o->grid_colored = g2;
-    if ((err = fit((const void*)k_volume<C, PH>, &o->grid_volume))) return err;
-    if ((err = fit((const void*)k_surface_uncolored<C, PH, true>, &o->grid_uncolored))) return err;
-    if ((err = fit((const void*)k_surface_uncolored<C, PH, false>, &g2))) return err;
-    if (g2 < o->grid_uncolored) o->grid_uncolored = g2;
+    if constexpr (T::OK) {
+      if ((err = fit((const void*)k_tpe_colored<C, PH, true>, T::SMEM, T::THREADS, &o->grid_colored))) return err;
+      if ((err = fit((const void*)k_tpe_colored<C, PH, false>, T::SMEM, T::THREADS, &g2))) return err;
+      if (g2 < o->grid_colored) o->grid_colored = g2;
+      if ((err = fit((const void*)k_tpe_volume<C, PH>, T::SMEM, T::THREADS, &o->grid_volume))) return err;
+      if ((err = fit((const void*)k_tpe_uncolored<C, PH, true>, T::SMEM, T::THREADS, &o->grid_uncolored))) return err;
+      if ((err = fit((const void*)k_tpe_uncolored<C, PH, false>, T::SMEM, T::THREADS, &g2))) return err;
+      if (g2 < o->grid_uncolored) o->grid_uncolored = g2;
+    } else {
+      if ((err = fit((const void*)k_surface_colored<C, PH, true>, C::SMEM, C::THREADS, &o->grid_colored))) return err;
+      if ((err = fit((const void*)k_surface_colored<C, PH, false>, C::SMEM, C::THREADS, &g2))) return err;
+      if (g2 < o->grid_colored) o->grid_colored = g2;
+      if ((err = fit((const void*)k_volume<C, PH>, C::VSMEM, C::THREADS, &o->grid_volume))) return err;
+      if ((err = fit((const void*)k_surface_uncolored<C, PH, true>, C::SMEM, C::THREADS, &o->grid_uncolored))) return err;
+      if ((err = fit((const void*)k_surface_uncolored<C, PH, false>, C::SMEM, C::THREADS, &g2))) return err;
+      if (g2 < o->grid_uncolored) o->grid_uncolored = g2;
+    }
     return cudaSuccess;
   }
   static Ops* ops() {
     static Ops o{C::DIM, C::NEQ, C::NP, C::NQF, C::NQV, C::NCODES, C::T_SIZE,
-                 int(C::T_SIZE * sizeof(double)), 0, 0, 0,
-                 &colored, &volume, &uncolored, &gather, &init};
+                 T::OK ? T::THREADS : C::THREADS, T::OK ? 16 : C::SPW,
+                 0, 0, 0, &colored, &volume, &uncolored, &gather, &init};
     return &o;
   }
 };
