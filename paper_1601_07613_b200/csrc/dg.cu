@@ -3,6 +3,7 @@
 // buffered / atomic RHS strategies and the fused SSP-RK3 stepper.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -17,6 +18,7 @@ struct mc_dg {
   mcdg::View view{};
   int n_colors = 0;
   std::vector<int64_t> bounds;
+  std::vector<char> has_first, has_last;   // per color: any first / last touch
   int64_t ne = 0, ng = 0, ns = 0, stride = 0;
   // device allocations
   int32_t *d_left = nullptr, *d_right = nullptr, *d_slots = nullptr;
@@ -62,7 +64,8 @@ int colored_pass(mc_dg* h, double* U, double* R, const mcdg::RK* rk, cudaStream_
   for (int c = 1; c <= h->n_colors; ++c) {
     const int64_t b = h->bounds[c - 1], e = h->bounds[c];
     if (e == b) continue;
-    DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, colored_grid(h, e - b), s));
+    DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, colored_grid(h, e - b), s,
+                           h->has_first[c], h->has_last[c]));
   }
   return MC_OK;
 }
@@ -107,10 +110,21 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
     if (e != cudaSuccess)
       return mc_fail(MC_ECUDA, std::string("kernel setup: ") + cudaGetErrorString(e));
   }
+  if (const char* g = std::getenv("MC_L2_FETCH")) {  // experiment knob (bytes)
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(std::atoi(g)));
+  }
   auto h = new mc_dg();
   h->ops = ops;
   h->n_colors = d->n_colors;
   h->bounds.assign(d->group_bounds, d->group_bounds + d->n_colors + 1);
+  h->has_first.assign(d->n_colors + 1, 0);
+  h->has_last.assign(d->n_colors + 1, 0);
+  for (int c = 1; c <= d->n_colors; ++c)
+    for (int64_t s = h->bounds[c - 1]; s < h->bounds[c]; ++s) {
+      const uint32_t code = d->surf_code[s];
+      if (code & (MC_FLAG_L_FIRST | MC_FLAG_R_FIRST)) h->has_first[c] = 1;
+      if (code & (MC_FLAG_L_LAST | MC_FLAG_R_LAST)) h->has_last[c] = 1;
+    }
   h->ne = d->n_elements;
   h->ng = d->n_ghosts;
   h->ns = d->n_surfaces;
@@ -222,11 +236,13 @@ MC_API int mc_dg_color_pass(mc_dg* h, int color, double* U, double* U0, double* 
   if (e == bb) return MC_OK;
   const int grid = colored_grid(h, e - bb);
   if (rk_mode == 0) {
-    DG_TRY(h->ops->colored(h->view, U, R, nullptr, bb, e, grid, as_stream(stream)));
+    DG_TRY(h->ops->colored(h->view, U, R, nullptr, bb, e, grid, as_stream(stream),
+                           h->has_first[color], h->has_last[color]));
   } else {
     if (!U0) return mc_fail(MC_EINVAL, "RK pass needs U0");
     mcdg::RK rk{U0, a, b, dt, rk_mode == 2 ? 1 : 0};
-    DG_TRY(h->ops->colored(h->view, U, R, &rk, bb, e, grid, as_stream(stream)));
+    DG_TRY(h->ops->colored(h->view, U, R, &rk, bb, e, grid, as_stream(stream),
+                           h->has_first[color], h->has_last[color]));
   }
   return MC_OK;
 }

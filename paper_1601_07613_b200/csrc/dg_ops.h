@@ -14,7 +14,7 @@ struct Ops {
   int spw;                                         // surfaces per warp
   int grid_colored, grid_volume, grid_uncolored;   // resident-grid sizes
   cudaError_t (*colored)(const View&, double* U, double* R, const RK* rk, int64_t b,
-                         int64_t e, int grid, cudaStream_t s);
+                         int64_t e, int grid, cudaStream_t s, bool has_first, bool has_last);
   cudaError_t (*volume)(const View&, const double* U, double* R, int grid, cudaStream_t s);
   cudaError_t (*uncolored)(const View&, const double* U, double* out, bool atomic, int grid,
                            cudaStream_t s);
@@ -33,12 +33,18 @@ struct Instance {
   using C = Cfg<K, PH, P>;
   using T = Tpe<C>;
   static cudaError_t colored(const View& v, double* U, double* R, const RK* rk, int64_t b,
-                             int64_t e, int grid, cudaStream_t s) {
+                             int64_t e, int grid, cudaStream_t s, bool has_first, bool has_last) {
     if constexpr (T::OK) {
-      if (rk)
-        k_tpe_colored<C, PH, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, *rk, b, e);
+      const bool krk = rk && has_last;
+      const RK r = rk ? *rk : RK{};
+      if (krk && has_first)
+        k_tpe_colored<C, PH, true, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
+      else if (krk)
+        k_tpe_colored<C, PH, true, false><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
+      else if (has_first)
+        k_tpe_colored<C, PH, false, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
       else
-        k_tpe_colored<C, PH, false><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, RK{}, b, e);
+        k_tpe_colored<C, PH, false, false><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
     } else {
       if (rk)
         k_surface_colored<C, PH, true><<<grid, C::THREADS, C::SMEM, s>>>(v, U, R, *rk, b, e);
@@ -93,9 +99,13 @@ struct Instance {
     cudaError_t err;
     int g2 = 0;
     if constexpr (T::OK) {
-      if ((err = fit((const void*)k_tpe_colored<C, PH, true>, T::SMEM, T::THREADS, &o->grid_colored))) return err;
-      if ((err = fit((const void*)k_tpe_colored<C, PH, false>, T::SMEM, T::THREADS, &g2))) return err;
-      if (g2 < o->grid_colored) o->grid_colored = g2;
+      if ((err = fit((const void*)k_tpe_colored<C, PH, true, true>, T::SMEM, T::THREADS, &o->grid_colored))) return err;
+      for (const void* fn : {(const void*)k_tpe_colored<C, PH, true, false>,
+                             (const void*)k_tpe_colored<C, PH, false, true>,
+                             (const void*)k_tpe_colored<C, PH, false, false>}) {
+        if ((err = fit(fn, T::SMEM, T::THREADS, &g2))) return err;
+        if (g2 < o->grid_colored) o->grid_colored = g2;
+      }
       if ((err = fit((const void*)k_tpe_volume<C, PH>, T::SMEM, T::THREADS, &o->grid_volume))) return err;
       if ((err = fit((const void*)k_tpe_uncolored<C, PH, true>, T::SMEM, T::THREADS, &o->grid_uncolored))) return err;
       if ((err = fit((const void*)k_tpe_uncolored<C, PH, false>, T::SMEM, T::THREADS, &g2))) return err;

@@ -29,7 +29,11 @@ struct Tpe {
   static constexpr bool OK = C::NEQ * C::NP <= 24;
   static constexpr int W = C::NEQ * C::NP;
   static constexpr int THREADS = 128;
+#ifdef MC_MINB_TPE
+  static constexpr int MINB = MC_MINB_TPE;
+#else
   static constexpr int MINB = (C::NEQ * C::NP > 16) ? 3 : 4;
+#endif
   static constexpr int SMEM = C::S_TOTAL * 8;
 };
 
@@ -267,7 +271,17 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 }
 
 // ------------------------------------------------------------- kernels
-template <class C, int PH, bool kRK>
+// L2 prefetch of a whole element block through the TMA engine (one
+// instruction per block; the data lands in L2 while the current tile
+// computes, so the next tile's loads hit L2 instead of waiting on HBM).
+__device__ __forceinline__ void prefetch_l2(const double* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
+// kVol: the color contains first touches (volume fused); kRK: the color
+// contains last touches of an RK stage (update fused).  The host picks the
+// variant per color launch so surface-only passes carry no volume code.
+template <class C, int PH, bool kRK, bool kVol>
 __global__ void __launch_bounds__(Tpe<C>::THREADS, Tpe<C>::MINB)
 k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
               int64_t end) {
@@ -277,11 +291,27 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
   const int lane = threadIdx.x & 31, side = lane & 1;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
+#ifdef MC_TPE_PREFETCH
+  const uint32_t blk = uint32_t(v.stride * 8);
+#endif
   for (int64_t tile = begin + warp * 16; tile < end; tile += nwarp * 16) {
     const int64_t s = tile + (lane >> 1);
+#ifdef MC_TPE_PREFETCH
+    {  // prefetch the next tile of this warp into L2
+      const int64_t sn = s + nwarp * 16;
+      if (sn < end) {
+        const int en = side ? __ldg(v.right + sn) : __ldg(v.left + sn);
+        if (en >= 0) {
+          prefetch_l2(U + int64_t(en) * v.stride, blk);
+          if (!kVol && en < v.n_elements) prefetch_l2(R + int64_t(en) * v.stride, blk);
+          if (kRK && rk.a != 0.0 && en < v.n_elements) prefetch_l2(rk.U0 + int64_t(en) * v.stride, blk);
+        }
+      }
+    }
+#endif
     const TpeSide t = tpe_side<C>(v, s, end, side);
-    const bool first = t.owner && (t.code & (side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
-    const bool last = t.owner && (t.code & (side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
+    const bool first = kVol && t.owner && (t.code & (side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
+    const bool last = kRK && t.owner && (t.code & (side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
     const int64_t off = int64_t(t.has ? t.e : 0) * v.stride;
     double u[W], acc[W];
     if (t.has) tload<W>(U + off, u);
@@ -294,10 +324,12 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
 #pragma unroll
       for (int j = 0; j < W; ++j) acc[j] = 0.0;
     }
-    if (first) tpe_volume<C, PH>(st, u, v.jinv + int64_t(t.e) * (C::DIM * C::DIM), v.prm, acc);
+    if constexpr (kVol) {
+      if (first) tpe_volume<C, PH>(st, u, v.jinv + int64_t(t.e) * (C::DIM * C::DIM), v.prm, acc);
+    }
     tpe_surface<C, PH>(st, t, side, u, v.prm, acc);
     if (t.owner) {
-      if (kRK && last) {
+      if (last) {
         if (rk.save_u0) tstore<W>(rk.U0 + off, u);
         if (rk.a != 0.0) {
           double u0[W];
