@@ -53,7 +53,9 @@ def config_spec(name: str):
         return dict(desc="2D Euler DG p=2, shuffle_elements(gen_tri_rect(708,708),0), LF, 3 colors",
                     build=lambda: P.shuffle_elements(P.gen_tri_rect(708, 708), 0),
                     physics="euler", p=2,
-                    sample=lambda: P.shuffle_elements(P.gen_tri_rect(177, 177), 0))
+                    sample=lambda: P.shuffle_elements(P.gen_tri_rect(177, 177), 0),
+                    # weak scaling: N stacked c2 slabs, one per GPU
+                    weak=lambda n: P.shuffle_elements(P.gen_tri_rect(708, 708 * n), 0))
     if name == "c3":
         return dict(desc="2D Euler DG p=3, gen_quad_rect(2000,2000), LF, 4 colors",
                     build=lambda: P.gen_quad_rect(2000, 2000), physics="euler", p=3,
@@ -82,14 +84,15 @@ def config_spec(name: str):
     raise SystemExit(f"unknown config {name}")
 
 
-def build_operator(spec, which="build"):
+def build_operator(spec, which="build", world=1, rank=0):
     from paper_1601_07613_b200.dg import DGOperator
     import paper_1601_07613_b200 as P
-    obj = spec[which]()
+    obj = spec["weak"](world) if (world > 1 and "weak" in spec) else spec[which]()
     if isinstance(obj, tuple):          # (RefinedMesh, 6-coloring)
         return DGOperator(obj[0], obj[1], degree=spec["p"], physics=spec["physics"])
     col, _ = P.color(obj)
-    return DGOperator(obj, col, degree=spec["p"], physics=spec["physics"])
+    return DGOperator(obj, col, degree=spec["p"], physics=spec["physics"], world=world,
+                      rank=rank)
 
 
 # ---------------------------------------------------------------- clocks
@@ -285,11 +288,11 @@ def main():
 
     spec = config_spec(args.config)
     t_setup = time.perf_counter()
-    op = build_operator(spec)
+    op = build_operator(spec, world=world, rank=rank)
     t_setup = time.perf_counter() - t_setup
     U_host = op.initial_state("wave")
     dt = op.stable_dt(0.2)
-    U = op.to_device(U_host)
+    U = torch.from_numpy(op.to_internal(U_host)).cuda()
     work = op.work_device()
     U0, R = work[0], work[1]
     stream = torch.cuda.current_stream()
@@ -297,6 +300,8 @@ def main():
 
     def step(events=None):
         for mode, a, b in STAGES:
+            if op.halo is not None:
+                op.halo.exchange(U)          # NCCL ghost exchange before each stage
             for c in range(1, nc + 1):
                 if events is not None:
                     ev = torch.cuda.Event(enable_timing=True)
@@ -329,8 +334,9 @@ def main():
         total_ms = float(t.item())
     ms_per_step = total_ms / max(args.steps, 1)
     ns, ne = op.n_surfaces, op.n_elements
-    value = world * 3 * ns / (ms_per_step * 1e-3)
-    dof_rate = world * ne * op.n_basis * op.n_equations * 3 / (ms_per_step * 1e-3)
+    ns_global, ne_global = op.mesh.n_surfaces, op.mesh.n_elements
+    value = 3 * ns_global / (ms_per_step * 1e-3)
+    dof_rate = ne_global * op.n_basis * op.n_equations * 3 / (ms_per_step * 1e-3)
 
     # per-launch durations of k_surface_colored from the timed region
     per = {}
@@ -360,21 +366,37 @@ def main():
     # correctness guard: the state must stay finite
     finite = bool(torch.isfinite(U).all().item())
 
-    # end-to-end through the public host-buffer API
-    pinned = torch.empty((ne, op.stride), dtype=torch.float64, pin_memory=True)
-    host = pinned.numpy()
-    host[:] = op.to_internal(U_host)
-    op.ssprk3_host_internal(host, dt, 1)          # warm (allocates scratch)
-    host[:] = op.to_internal(U_host)
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        op.ssprk3_host_internal(host, dt, 1)
-    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-    e2e_value = world * 3 * ns / e2e_s
-    state_bytes = ne * op.stride * 8
+    # end-to-end through the public host-buffer API (H2D state, step, D2H state)
+    state_bytes = op.n_local * op.stride * 8
+    if world == 1:
+        pinned = torch.empty((ne, op.stride), dtype=torch.float64, pin_memory=True)
+        host = pinned.numpy()
+        host[:] = op.to_internal(U_host)
+        op.ssprk3_host_internal(host, dt, 1)          # warm (allocates scratch)
+        host[:] = op.to_internal(U_host)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            op.ssprk3_host_internal(host, dt, 1)
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    else:
+        pinned = torch.empty((op.n_local, op.stride), dtype=torch.float64, pin_memory=True)
+        pinned.copy_(torch.from_numpy(op.to_internal(U_host)))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            U.copy_(pinned, non_blocking=True)
+            op.ssprk3_distributed(U, work, dt, 1)
+            pinned.copy_(U, non_blocking=True)
+            torch.cuda.synchronize()
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = 3 * ns_global / e2e_s
 
     comparisons = None
-    if args.variants:
+    if args.variants and world == 1:
         comparisons = variants(op, U_host, spec, stream)
 
     cpu = None
@@ -389,18 +411,22 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (density wave on far-field stream)",
-        "config": {"workload": spec["desc"], "elements": ne, "surfaces": ns, "colors": nc,
+        "config": {"workload": spec["desc"] + ("" if world == 1 else
+                                               f", weak-scaled to {world} stacked slabs"),
+                   "elements": ne_global, "surfaces": ns_global, "colors": nc,
                    "degree": op.degree, "n_basis": op.n_basis, "n_equations": op.n_equations,
                    "step": "1 SSP-RK3 step = 3 fused colored RHS (volume fused into first "
                            "color pass, RK update into last)",
                    "l2": f"inputs larger than L2 (state {state_bytes / 1e9:.2f} GB x 3 arrays)",
-                   "parallelism": "single-GPU" if world == 1 else f"replicas x{world}",
+                   "parallelism": "single-GPU" if world == 1 else
+                   f"domain decomposition x{world} (y slabs, NCCL ghost exchange per stage)",
                    "setup_s": round(t_setup, 2)},
         "dof_updates_per_s": dof_rate,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "frac_of_8tbs_nominal": achieved / 8000.0,
-                     "kernel": "k_surface_colored",
+                     "kernel": ("k_tpe_colored" if op.n_equations * op.n_basis <= 24
+                                else "k_surface_colored"),
                      "algorithmic_bytes_per_step": bytes_step,
                      "kernel_ms_per_step": ms_step,
                      "per_color_gbs": {str(c): v[0] / (v[1] * 1e-3) / 1e9
@@ -427,7 +453,7 @@ def variants(op, U_host, spec, stream, reps=5):
     import paper_1601_07613_b200 as P
     from paper_1601_07613_b200.sweeps import DeviceLayout
     out = {}
-    U = op.to_device(U_host)
+    U = torch.from_numpy(op.to_internal(U_host)).cuda()
     R = torch.zeros_like(U)
 
     def timeit(fn):

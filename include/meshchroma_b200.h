@@ -151,6 +151,10 @@ int mc_default_payload_dev(int64_t n, int64_t seed, int64_t* out_dev,
 #define MC_FLAG_R_FIRST (1u << 14)
 #define MC_FLAG_R_LAST (1u << 15)
 #define MC_FLAG_R_GHOST (1u << 16)
+/* sides swapped w.r.t. the canonical (single-domain) orientation by the
+ * partitioner: the flux is evaluated in canonical orientation so owned
+ * residuals stay bit-identical to the single-domain run */
+#define MC_FLAG_FLIPPED (1u << 17)
 
 typedef struct mc_dg_desc {
   int kind;        /* MC_KIND_* */

@@ -585,7 +585,8 @@ __device__ __forceinline__ void surface_tasks(const double* st, double* ws, cons
   const double* fphi = st + C::S_FPHI + c.mycode * (C::NQF * C::NPP);
   const double* fw = st + C::S_FW;
   int* valid = reinterpret_cast<int*>(ws + C::W_FLAG);
-  if (ln.active && ln.side == 0 && ln.eq == 0) valid[ln.grp] = c.valid;
+  if (ln.active && ln.side == 0 && ln.eq == 0)
+    valid[ln.grp] = c.valid ? ((c.code & MC_FLAG_FLIPPED) ? 2 : 1) : 0;
   if (ln.active) {
 #pragma unroll 1
     for (int g = 0; g < C::NQF; ++g) {
@@ -611,8 +612,18 @@ __device__ __forceinline__ void surface_tasks(const double* st, double* ws, cons
       }
 #pragma unroll
       for (int d = 0; d < C::DIM; ++d) n[d] = ws[C::W_NRM + gs * C::DIM + d];
-      Physics<PH, C::DIM, C::NEQ>::lf(sL, sR, n, prm, out);
-      const double w = fw[g];
+      // flipped by the partitioner: canonical orientation, one call site
+      const bool flip = valid[gs] == 2;
+      double cL[C::NEQ], cR[C::NEQ];
+#pragma unroll
+      for (int k = 0; k < C::NEQ; ++k) {
+        cL[k] = flip ? sR[k] : sL[k];
+        cR[k] = flip ? sL[k] : sR[k];
+      }
+#pragma unroll
+      for (int d = 0; d < C::DIM; ++d) n[d] = flip ? -n[d] : n[d];
+      Physics<PH, C::DIM, C::NEQ>::lf(cL, cR, n, prm, out);
+      const double w = flip ? -fw[g] : fw[g];
 #pragma unroll
       for (int k = 0; k < C::NEQ; ++k) ws[C::W_FS + t * C::SV + k] = w * out[k];
     }

@@ -183,9 +183,21 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
       sL[k] = side ? other : own[k];
       sR[k] = side ? own[k] : other;
     }
-    Physics<PH, C::DIM, NEQ>::lf(sL, sR, t.n, P, out);
+    // canonical (single-domain) orientation for partitioner-flipped surfaces,
+    // through ONE call site so the arithmetic is bit-identical to 1 domain
+    const bool flip = (t.code & MC_FLAG_FLIPPED) != 0;
+    double cL[NEQ], cR[NEQ], nn[C::DIM];
+#pragma unroll
+    for (int k = 0; k < NEQ; ++k) {
+      cL[k] = flip ? sR[k] : sL[k];
+      cR[k] = flip ? sL[k] : sR[k];
+    }
+#pragma unroll
+    for (int d = 0; d < C::DIM; ++d) nn[d] = flip ? -t.n[d] : t.n[d];
+    Physics<PH, C::DIM, NEQ>::lf(cL, cR, nn, P, out);
+    double c = sc * fw[g];
+    if (flip) c = -c;
     if (t.owner) {
-      const double c = sc * fw[g];
 #pragma unroll
       for (int k = 0; k < NEQ; ++k) {
         const double f = c * out[k];

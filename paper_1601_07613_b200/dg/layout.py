@@ -44,6 +44,7 @@ FLAG_L_LAST = 1 << 13
 FLAG_R_FIRST = 1 << 14
 FLAG_R_LAST = 1 << 15
 FLAG_R_GHOST = 1 << 16
+FLAG_FLIPPED = 1 << 17
 
 
 def mesh_kind(mesh: Mesh) -> ElementKind:
@@ -175,7 +176,7 @@ def _normals(kind, Xl, local_l, surf_pts_l, centroid):
 
 
 def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
-                       period=None, mortars=None, owned=None) -> SurfaceList:
+                       period=None, mortars=None, owned=None, flipped=None) -> SurfaceList:
     """Assemble the device surface list from a color-grouped mesh.
 
     ``colors`` must be non-decreasing over surface ids (a mesh produced by
@@ -285,10 +286,13 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
     code |= np.where(first[L] == col, FLAG_L_FIRST, 0)
     code |= np.where(last[L] == col, FLAG_L_LAST, 0)
     rr = np.where(has_r, R, 0)
-    code |= np.where(has_r & (first[rr] == col), FLAG_R_FIRST, 0)
-    code |= np.where(has_r & (last[rr] == col), FLAG_R_LAST, 0)
     ghost_r = has_r & (R >= ne)
+    own_r = has_r & ~ghost_r          # ghosts are never finalised: no flags
+    code |= np.where(own_r & (first[rr] == col), FLAG_R_FIRST, 0)
+    code |= np.where(own_r & (last[rr] == col), FLAG_R_LAST, 0)
     code |= np.where(ghost_r, FLAG_R_GHOST, 0)
+    if flipped is not None:
+        code |= np.where(np.asarray(flipped)[sid], FLAG_FLIPPED, 0)
     if (L >= ne).any():
         raise ValueError("left elements must be owned")
 

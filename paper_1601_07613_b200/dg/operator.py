@@ -65,7 +65,8 @@ def ordering_plan(mesh: Mesh, coloring: SurfaceColoring, ordering: str) -> Reord
 class DGOperator:
     def __init__(self, mesh, coloring: SurfaceColoring | None = None, degree: int = 1,
                  physics: str = "euler", *, period=None, gamma: float = 1.4,
-                 velocity=(1.0, 0.5, 0.25), farfield=None, ordering: str = "reorder"):
+                 velocity=(1.0, 0.5, 0.25), farfield=None, ordering: str = "reorder",
+                 world: int = 1, rank: int = 0):
         mortars = None
         if isinstance(mesh, RefinedMesh):
             mortars = mesh.hanging_array()
@@ -96,13 +97,33 @@ class DGOperator:
         self.layout_coloring = lcol
         if mortars is not None and len(mortars):
             mortars = self.plan.surface_perm[mortars]
-        self.surfaces = build_surface_list(self.layout_mesh, lcol.colors, lcol.n_colors,
-                                           period=period, mortars=mortars)
         self.mortars = mortars
+        self.world, self.rank, self.part = int(world), int(rank), None
+        if self.world > 1:
+            # domain decomposition of the renumbered mesh (partition.py)
+            from ..partition import HaloExchange, build_partition, slab_owner
+            if mortars is not None and len(mortars):
+                raise NotImplementedError("partitioned AMR meshes are not supported yet")
+            owner = slab_owner(self.layout_mesh, self.world, period=period)
+            self.part = build_partition(self.layout_mesh, lcol.colors, lcol.n_colors, owner,
+                                        self.rank)
+            self.surfaces = build_surface_list(self.part.mesh, self.part.colors, lcol.n_colors,
+                                               period=period, owned=self.part.n_owned,
+                                               flipped=self.part.flipped)
+            self.n_elements = self.part.n_owned
+            self.n_local = self.part.n_local
+        else:
+            self.surfaces = build_surface_list(self.layout_mesh, lcol.colors, lcol.n_colors,
+                                               period=period, mortars=mortars)
+            self.n_elements = mesh.n_elements
+            self.n_local = mesh.n_elements
         self.tables = reference_tables(self.kind, self.degree)
         self.n_basis = self.tables.n_basis
-        self.n_elements = mesh.n_elements
         self._create()
+        self.halo = None
+        if self.part is not None:
+            from ..partition import HaloExchange
+            self.halo = HaloExchange(self.part, "cuda")
 
     # ---------------------------------------------------------- native
     def _create(self):
@@ -166,11 +187,27 @@ class DGOperator:
         return self.n_equations * self.n_basis
 
     def to_internal(self, U: np.ndarray) -> np.ndarray:
-        """(ne, neq, nb) user order -> (ne, stride) renumbered, padded."""
-        U = np.asarray(U, dtype=np.float64).reshape(self.n_elements, -1)
+        """(ne, neq, nb) user order -> (n_local, stride) renumbered, padded.
+        On a partitioned operator: this rank's owned rows (ghost rows zero
+        until the first halo exchange)."""
+        U = np.asarray(U, dtype=np.float64).reshape(self.mesh.n_elements, -1)
+        if self.part is not None:
+            inv = np.empty_like(self.plan.element_perm)
+            inv[self.plan.element_perm] = np.arange(len(inv))
+            out = np.zeros((self.n_local, self.stride))
+            out[: self.n_elements, : self.block_width()] = U[inv[self.part.owned]]
+            return out
         out = np.zeros((self.n_elements, self.stride))
         out[self.plan.element_perm, : self.block_width()] = U
         return out
+
+    def owned_user_ids(self) -> np.ndarray:
+        """Original (user) element ids of this rank's internal rows."""
+        inv = np.empty_like(self.plan.element_perm)
+        inv[self.plan.element_perm] = np.arange(len(inv))
+        if self.part is None:
+            return inv
+        return inv[self.part.owned]
 
     def from_internal(self, B: np.ndarray) -> np.ndarray:
         B = np.asarray(B).reshape(self.n_elements, self.stride)
@@ -179,7 +216,7 @@ class DGOperator:
 
     def empty_device(self):
         import torch
-        return torch.zeros((self.n_elements, self.stride), dtype=torch.float64, device="cuda")
+        return torch.zeros((self.n_local, self.stride), dtype=torch.float64, device="cuda")
 
     def to_device(self, U: np.ndarray):
         import torch
@@ -208,7 +245,21 @@ class DGOperator:
 
     def work_device(self):
         import torch
-        return torch.zeros((2, self.n_elements, self.stride), dtype=torch.float64, device="cuda")
+        return torch.zeros((2, self.n_local, self.stride), dtype=torch.float64, device="cuda")
+
+    STAGES = ((2, 0.0, 1.0), (1, 0.75, 0.25), (1, 1.0 / 3.0, 2.0 / 3.0))
+
+    def ssprk3_distributed(self, U_dev, work_dev, dt: float, steps: int = 1, stream=None) -> None:
+        """SSP-RK3 on a partitioned operator: ghost exchange before every
+        stage, then the stage's color launches (volume fused into first
+        touch, update into last touch, U0 saved in stage 1)."""
+        U0, R = work_dev[0], work_dev[1]
+        for _ in range(steps):
+            for mode, a, b in self.STAGES:
+                if self.halo is not None:
+                    self.halo.exchange(U_dev)
+                for c in range(1, self.n_colors + 1):
+                    self.color_pass_device(c, U_dev, U0, R, mode, a, b, dt, stream)
 
     def ssprk3_device(self, U_dev, work_dev, dt: float, steps: int = 1, stream=None) -> None:
         _native.check(self._lib.mc_dg_ssprk3(self._h, _native.ptr(U_dev), _native.ptr(work_dev),
