@@ -292,6 +292,11 @@ def main():
     t_setup = time.perf_counter() - t_setup
     U_host = op.initial_state("wave")
     dt = op.stable_dt(0.2)
+    if world > 1:                      # one global time step; also initialises NCCL P2P
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        dt = float(t.item())
+        dist.barrier()
     U = torch.from_numpy(op.to_internal(U_host)).cuda()
     work = op.work_device()
     U0, R = work[0], work[1]

@@ -79,10 +79,20 @@ def element_geometry(kind: ElementKind, X: np.ndarray):
     else:
         d = DIM[kind]
         J = np.stack([X[:, r + 1] - X[:, 0] for r in range(d)], axis=2)
-    det = np.linalg.det(J)
+    # closed-form determinant / inverse (batched LAPACK is slow at 10^7 elements)
+    if J.shape[1] == 2:
+        a, b, c, d = J[:, 0, 0], J[:, 0, 1], J[:, 1, 0], J[:, 1, 1]
+        det = a * d - b * c
+        inv = np.stack([np.stack([d, -b], 1), np.stack([-c, a], 1)], 1)
+    else:
+        c0 = np.cross(J[:, :, 1], J[:, :, 2])
+        c1 = np.cross(J[:, :, 2], J[:, :, 0])
+        c2 = np.cross(J[:, :, 0], J[:, :, 1])
+        det = (J[:, :, 0] * c0).sum(1)
+        inv = np.stack([c0, c1, c2], 1)          # rows of J^-1 * det
     if (np.abs(det) < 1e-300).any():
         raise ValueError("degenerate element")
-    return det, np.linalg.inv(J)
+    return det, inv / det[:, None, None]
 
 
 def _side_codes_2d(kind, elem_verts, elems, local, surf_verts, mids=None):
@@ -225,14 +235,14 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
     L, R, col = L[sid], R[sid], colors[sid]
     sv = mesh.surf_verts[sid]
 
-    # race certificate including mortar coupling
+    # race certificate including mortar coupling (O(n) counting per color)
     for c in range(1, n_colors + 1):
         m = col == c
         touched = np.concatenate([L[m], R[m & (R >= 0)]])
-        u, cnt = np.unique(touched, return_counts=True)
+        cnt = np.bincount(touched, minlength=ne_all)
         if (cnt > 1).any():
-            raise WriteConflictError(
-                f"color {c} writes element {int(u[cnt > 1][0])} {int(cnt[cnt > 1][0])} times")
+            e = int(np.flatnonzero(cnt > 1)[0])
+            raise WriteConflictError(f"color {c} writes element {e} {int(cnt[e])} times")
 
     loc_l = _local_side(mesh, L, sid)
     has_r = R >= 0
@@ -275,12 +285,17 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
     # first / last touch per element over the color sequence (owned only)
     code = (code_l | (code_r << 6)).astype(np.int64)
     big = n_colors + 1
-    first = np.full(ne_all, big, dtype=np.int64)
-    last = np.zeros(ne_all, dtype=np.int64)
-    np.minimum.at(first, L, col)
-    np.maximum.at(last, L, col)
-    np.minimum.at(first, R[has_r], col[has_r])
-    np.maximum.at(last, R[has_r], col[has_r])
+    # first / last color per element from its side list (+ mortar halves)
+    pos = np.full(mesh.n_surfaces, -1, dtype=np.int64)
+    pos[sid] = np.arange(len(sid))
+    es = mesh.elem_surfs
+    ent = np.where(es >= 0, pos[np.where(es >= 0, es, 0)], -1)
+    ecol = np.where(ent >= 0, col[np.where(ent >= 0, ent, 0)], -1)
+    first = np.where(ecol >= 1, ecol, big).min(axis=1)
+    last = ecol.max(axis=1).clip(min=0)
+    if mortar_r.any():                 # coarse elements also see the mortar halves
+        np.minimum.at(first, R[mortar_r], col[mortar_r])
+        np.maximum.at(last, R[mortar_r], col[mortar_r])
     if (first[:ne] == big).any():
         raise ValueError("element without surfaces")
     code |= np.where(first[L] == col, FLAG_L_FIRST, 0)
@@ -306,7 +321,7 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
     elem = np.concatenate([L, R[own_r]])
     slot = np.concatenate([2 * ent, 2 * ent[own_r] + 1])
     rank = np.concatenate([loc_l, loc_r[own_r] + 4 * mortar_r[own_r]])
-    order = np.lexsort((slot, rank, elem))
+    order = np.argsort(elem * 16 + rank, kind="stable")   # slots ascend within ties
     elem, slot = elem[order], slot[order]
     ptr = np.zeros(ne + 1, dtype=np.int64)
     ptr[1:] = np.cumsum(np.bincount(elem, minlength=ne)[:ne])
