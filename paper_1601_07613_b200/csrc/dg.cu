@@ -3,6 +3,7 @@
 // buffered / atomic RHS strategies and the fused SSP-RK3 stepper.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -23,7 +24,7 @@ struct mc_dg {
   // device allocations
   int32_t *d_left = nullptr, *d_right = nullptr, *d_slots = nullptr;
   uint32_t* d_code = nullptr;
-  double *d_geom = nullptr, *d_jinv = nullptr, *d_tables = nullptr;
+  double *d_geom = nullptr, *d_jinv = nullptr, *d_tables = nullptr, *d_ptables = nullptr;
   int64_t* d_slot_ptr = nullptr;
   double* d_buffer = nullptr;      // 2*ns blocks (buffered strategy)
   double* d_host_U = nullptr;      // host path scratch: U, U0, R
@@ -56,7 +57,8 @@ int colored_grid(const mc_dg* h, int64_t n) {
   const int64_t wpb = h->ops->threads / 32;
   const int64_t max_blocks = (tiles + wpb - 1) / wpb;
   int grid = h->ops->grid_colored;
-  if (grid > max_blocks) grid = int(max_blocks);
+  static const bool full = std::getenv("MC_FULL_GRID") != nullptr;   // A/B knob
+  if (full || grid > max_blocks) grid = int(std::min<int64_t>(max_blocks, 1 << 30));
   return grid < 1 ? 1 : grid;
 }
 
@@ -159,7 +161,15 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
     mc_dg_destroy(h);
     return mc_fail(MC_ENOMEM, std::string("DG upload: ") + cudaGetErrorString(e));
   }
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_ptables, sizeof(double) * size_t(ops->stable_size));
+  if (e == cudaSuccess) e = ops->stage_global(h->d_tables, h->d_ptables, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    mc_dg_destroy(h);
+    return mc_fail(MC_ECUDA, std::string("DG table staging: ") + cudaGetErrorString(e));
+  }
   mcdg::View& v = h->view;
+  v.ptables = h->d_ptables;
   v.left = h->d_left;
   v.right = h->d_right;
   v.code = h->d_code;
@@ -186,6 +196,7 @@ MC_API int mc_dg_destroy(mc_dg* h) {
   cudaFree(h->d_geom);
   cudaFree(h->d_jinv);
   cudaFree(h->d_tables);
+  cudaFree(h->d_ptables);
   cudaFree(h->d_slot_ptr);
   cudaFree(h->d_slots);
   cudaFree(h->d_buffer);

@@ -158,6 +158,7 @@ struct View {
   const double* geom;
   const double* jinv;
   const double* tables;
+  const double* ptables;   // padded shared-memory layout, in global memory (L1-cached reads)
   const int64_t* slot_ptr;
   const int32_t* slots;
   int64_t n_elements;

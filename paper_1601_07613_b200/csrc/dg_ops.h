@@ -20,6 +20,8 @@ struct Ops {
                            cudaStream_t s);
   cudaError_t (*gather)(const View&, const double* buf, double* R, cudaStream_t s);
   cudaError_t (*init)(Ops* self);   // occupancy queries, smem opt-in
+  int stable_size;                  // doubles of the padded table layout
+  cudaError_t (*stage_global)(const double* tables, double* out, cudaStream_t s);
 };
 
 // defined in dg_tri.cu / dg_quad.cu / dg_tet.cu; nullptr if not compiled
@@ -121,10 +123,19 @@ struct Instance {
     }
     return cudaSuccess;
   }
+  static cudaError_t stage_global(const double* tables, double* out, cudaStream_t s) {
+    const int smem = C::S_TOTAL * 8;
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_stage_global<C>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k_stage_global<C><<<1, 256, smem, s>>>(tables, out);
+    return cudaGetLastError();
+  }
   static Ops* ops() {
     static Ops o{C::DIM, C::NEQ, C::NP, C::NQF, C::NQV, C::NCODES, C::T_SIZE,
                  T::OK ? T::THREADS : C::THREADS, T::OK ? 16 : C::SPW,
-                 0, 0, 0, &colored, &volume, &uncolored, &gather, &init};
+                 0, 0, 0, &colored, &volume, &uncolored, &gather, &init, C::S_TOTAL,
+                 &stage_global};
     return &o;
   }
 };

@@ -293,13 +293,24 @@ __device__ __forceinline__ void prefetch_l2(const double* p, uint32_t bytes) {
 // kVol: the color contains first touches (volume fused); kRK: the color
 // contains last touches of an RK stage (update fused).  The host picks the
 // variant per color launch so surface-only passes carry no volume code.
+#ifndef MC_TPE_GLOBAL_TABLES
+#define MC_TPE_GLOBAL_TABLES 0
+#endif
+#ifndef MC_TPE_MINB_SURF
+#define MC_TPE_MINB_SURF 3
+#endif
 template <class C, int PH, bool kRK, bool kVol>
-__global__ void __launch_bounds__(Tpe<C>::THREADS, Tpe<C>::MINB)
+__global__ void __launch_bounds__(Tpe<C>::THREADS, kVol ? Tpe<C>::MINB : MC_TPE_MINB_SURF)
 k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
               int64_t end) {
   constexpr int W = Tpe<C>::W;
-  extern __shared__ double st[];
-  tpe_stage<C>(v.tables, st);
+#if MC_TPE_GLOBAL_TABLES
+  const double* st = v.ptables;          // 4-30 KB, stays L1/L2 resident
+#else
+  extern __shared__ double sts[];
+  tpe_stage<C>(v.tables, sts);
+  const double* st = sts;
+#endif
   const int lane = threadIdx.x & 31, side = lane & 1;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -413,6 +424,15 @@ k_tpe_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
     tpe_volume<C, PH>(st, u, v.jinv + e * (C::DIM * C::DIM), v.prm, acc);
     tstore<W>(R + e * v.stride, acc);
   }
+}
+
+// Write the padded table layout (what tpe_stage puts in shared memory) to
+// global memory once per operator; kernels may read it through L1.
+template <class C>
+__global__ void k_stage_global(const double* __restrict__ g, double* out) {
+  extern __shared__ double sts[];
+  stage_tables<C>(g, sts);
+  for (int i = threadIdx.x; i < C::S_TOTAL; i += blockDim.x) out[i] = sts[i];
 }
 
 }  // namespace mcdg
