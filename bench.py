@@ -185,6 +185,16 @@ def launch_bytes(op, color: int, rk_mode: int, a: float) -> int:
 STAGES = ((2, 0.0, 1.0), (1, 0.75, 0.25), (1, 1.0 / 3.0, 2.0 / 3.0))
 
 
+def kernel_name(op) -> str:
+    """Which colored kernel the library dispatches (csrc/dg_tpe.cuh Tpe::OK)."""
+    w = op.n_equations * op.n_basis
+    if w <= 24:
+        return "k_tpe_colored (1 lane per element side)"
+    if w <= 64 and op.dim == 2 and op.n_equations >= 2:
+        return "k_tpe_colored (2 lanes per element side)"
+    return "k_surface_colored (2*N_eq lanes per surface, warp flux tasks)"
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -430,8 +440,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "frac_of_8tbs_nominal": achieved / 8000.0,
-                     "kernel": ("k_tpe_colored" if op.n_equations * op.n_basis <= 24
-                                else "k_surface_colored"),
+                     "kernel": kernel_name(op),
                      "algorithmic_bytes_per_step": bytes_step,
                      "kernel_ms_per_step": ms_step,
                      "per_color_gbs": {str(c): v[0] / (v[1] * 1e-3) / 1e9

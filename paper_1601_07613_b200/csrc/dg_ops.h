@@ -133,7 +133,7 @@ struct Instance {
   }
   static Ops* ops() {
     static Ops o{C::DIM, C::NEQ, C::NP, C::NQF, C::NQV, C::NCODES, C::T_SIZE,
-                 T::OK ? T::THREADS : C::THREADS, T::OK ? 16 : C::SPW,
+                 T::OK ? T::THREADS : C::THREADS, T::OK ? T::SW : C::SPW,
                  0, 0, 0, &colored, &volume, &uncolored, &gather, &init, C::S_TOTAL,
                  &stage_global};
     return &o;

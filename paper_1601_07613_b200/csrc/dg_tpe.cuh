@@ -1,20 +1,24 @@
-// Thread-per-element-side DG kernels for small element blocks
-// (N_eq * N_p <= 24 doubles: c1 advection p=1, c2 Euler p=2 on triangles,
-// Euler p=1 on quads, ...).
+// Register-resident DG kernels: H lanes per element side (H = 1 or 2).
 //
-// Each lane owns a WHOLE element block in registers: lanes (2i, 2i+1) are
-// the left / right side of surface i, 16 surfaces per warp.  A lane loads
-// its element's coefficients with 16-byte loads (high memory-level
-// parallelism: the whole block is in flight at once), evaluates its own
-// traces, swaps them with its partner through one shuffle per equation,
-// evaluates the Lax-Friedrichs flux (both partners compute the same value),
-// lifts it into its own residual block and stores.  In the first-touch pass
-// it also evaluates the element's volume integral (one flux per volume
-// point, no redundancy).  Reference-element tables live in shared memory
-// and are read either as warp-wide broadcasts (volume tables) or per lane
-// (face tables, indexed by the side code).  No shared-memory staging of
-// per-element data at all — this is what the smem-bound group kernel
-// (dg_kernels.cuh) cannot avoid.
+// Lanes (2H*i + H*side + h) serve surface i of a warp (16/H surfaces per
+// warp): `side` picks the left / right element, `h` picks an equation group
+// (equations [h*NEQH, min(NEQ, (h+1)*NEQH)) ), so a lane holds NEQH*N_p
+// coefficients of ONE element in registers:
+//   H = 1 when N_eq*N_p <= 24 (c1, c2 Euler p=2 triangles, quad p=1, ...):
+//         the whole block, 256-bit loads/stores;
+//   H = 2 when N_eq*N_p <= 64 (c3 quad p=3, c4 tet p=2, ...): an equation
+//         group, 128-bit loads/stores.
+// Per quadrature point a lane evaluates the traces of its own equations,
+// assembles the full state of its side from its sibling and the other
+// side's state from the partner lane (warp shuffles), evaluates the
+// Lax-Friedrichs flux (all 2H lanes of a surface compute the same value —
+// redundant but register-only), and lifts its own equations into its
+// residual block.  In the first-touch pass it also evaluates the element's
+// volume integral the same way.  Reference-element tables live in shared
+// memory (volume tables are warp-wide broadcasts, face tables are indexed by
+// the side code); no per-element data ever goes through shared memory,
+// which is what keeps these kernels off the shared-memory roofline that
+// bounds the group kernel (dg_kernels.cuh).
 //
 // Same accumulation order per element as Algorithm 1 and the oracle:
 // volume, then colors 1..n; within a surface the quadrature points in order.
@@ -26,20 +30,32 @@ namespace mcdg {
 
 template <class C>
 struct Tpe {
-  static constexpr bool OK = C::NEQ * C::NP <= 24;
   static constexpr int W = C::NEQ * C::NP;
+  static constexpr int H = (W <= 24) ? 1 : ((W <= 64 && C::NEQ >= 2) ? 2 : 0);
+  static constexpr int NEQH = H ? (C::NEQ + H - 1) / H : C::NEQ;   // eqs of lane h = 0
+  static constexpr int NEQ1 = C::NEQ - NEQH;                       // eqs of lane h = 1
+  static constexpr int WH = NEQH * C::NP;                          // doubles per lane
+  // H = 2 moves 16-byte pairs: every lane's run must have even length
+  static constexpr bool PAIRS = (C::NP % 2 == 0) || (NEQH % 2 == 0 && NEQ1 % 2 == 0);
+#ifdef MC_TPE_H1_ONLY
+  static constexpr bool OK = H == 1;
+#else
+  // tets keep the group kernel: with 27 volume points the 2x redundant flux
+  // of H = 2 loses to the task scheme (measured)
+  static constexpr bool OK = H == 1 || (H == 2 && PAIRS && C::DIM == 2);
+#endif
+  static constexpr int SW = 16 / (H ? H : 1);                      // surfaces per warp
   static constexpr int THREADS = 128;
 #ifdef MC_MINB_TPE
   static constexpr int MINB = MC_MINB_TPE;
 #else
-  static constexpr int MINB = (C::NEQ * C::NP > 16) ? 3 : 4;
+  static constexpr int MINB = (H == 2) ? 2 : ((W > 16) ? 3 : 4);
 #endif
   static constexpr int SMEM = C::S_TOTAL * 8;
 };
 
-// sum_j row[j] * u[off + j]
-template <int NP, int W>
-__device__ __forceinline__ double tdot(const double* row, const double (&u)[W], int off) {
+template <int NP, int N>
+__device__ __forceinline__ double tdot(const double* row, const double (&u)[N], int off) {
   const double2* r2 = reinterpret_cast<const double2*>(row);
   double t = 0.0;
 #pragma unroll
@@ -52,8 +68,8 @@ __device__ __forceinline__ double tdot(const double* row, const double (&u)[W], 
   return t;
 }
 
-template <int NP, int W>
-__device__ __forceinline__ void taxpy(const double* row, double f, double (&acc)[W], int off) {
+template <int NP, int N>
+__device__ __forceinline__ void taxpy(const double* row, double f, double (&acc)[N], int off) {
   const double2* r2 = reinterpret_cast<const double2*>(row);
 #pragma unroll
   for (int j = 0; j < NP / 2; ++j) {
@@ -64,12 +80,44 @@ __device__ __forceinline__ void taxpy(const double* row, double f, double (&acc)
   if constexpr (NP % 2) acc[off + NP - 1] = fma(row[NP - 1], f, acc[off + NP - 1]);
 }
 
-// Volume integral of one element (this lane), added into acc.
+// Full state of this side at one point from the lanes' own traces.
+template <class C>
+__device__ __forceinline__ void assemble_state(const double (&own)[Tpe<C>::NEQH], int h,
+                                               double (&s)[C::NEQ]) {
+  constexpr int NEQH = Tpe<C>::NEQH;
+  if constexpr (Tpe<C>::H == 1) {
+#pragma unroll
+    for (int k = 0; k < C::NEQ; ++k) s[k] = own[k];
+  } else {
+    double oth[NEQH];
+#pragma unroll
+    for (int k = 0; k < NEQH; ++k) oth[k] = __shfl_xor_sync(kFull, own[k], 1);
+#pragma unroll
+    for (int e = 0; e < C::NEQ; ++e)
+      s[e] = (e < NEQH) ? (h == 0 ? own[e] : oth[e])
+                        : (h == 1 ? own[e - NEQH] : oth[e - NEQH]);
+  }
+}
+
+// This lane's k-th equation of a full NEQ vector.
+template <class C>
+__device__ __forceinline__ double own_part(const double* v, int h, int k) {
+  constexpr int NEQH = Tpe<C>::NEQH;
+  if constexpr (Tpe<C>::H == 1) {
+    return v[k];
+  } else {
+    const int e1 = (NEQH + k < C::NEQ) ? NEQH + k : C::NEQ - 1;
+    return h == 0 ? v[k] : v[e1];
+  }
+}
+
+// Volume integral of this lane's element (its equations), added into acc.
 template <class C, int PH>
-__device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[Tpe<C>::W],
-                                           const double* __restrict__ jinv_e, const Params& P,
-                                           double (&acc)[Tpe<C>::W]) {
-  constexpr int W = Tpe<C>::W, NP = C::NP, NEQ = C::NEQ, DIM = C::DIM;
+__device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[Tpe<C>::WH],
+                                           const double* __restrict__ jinv_e, int h, int nown,
+                                           bool mine, const Params& P,
+                                           double (&acc)[Tpe<C>::WH]) {
+  constexpr int WH = Tpe<C>::WH, NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH, DIM = C::DIM;
   const double* vphi = st + C::S_VPHI;
   const double* vdphi = st + C::S_VDPHI;
   const double* vw = st + C::S_VW;
@@ -78,11 +126,13 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
 #pragma unroll 1
   for (int q = 0; q < C::NQV; ++q) {
-    double s[NEQ];
+    double own[NEQH], s[NEQ];
 #pragma unroll
-    for (int k = 0; k < NEQ; ++k) s[k] = tdot<NP, W>(vphi + q * C::NPP, u, k * NP);
+    for (int k = 0; k < NEQH; ++k) own[k] = tdot<NP, WH>(vphi + q * C::NPP, u, k * NP);
+    assemble_state<C>(own, h, s);
     const double w = vw[q];
-    if constexpr (PH == EULER) {
+    if constexpr (Tpe<C>::H == 1 && PH == EULER) {
+      // whole block in this lane: fluxes straight into the projection
       const double inv = 1.0 / s[0];
       double vel[DIM], ke = 0.0;
 #pragma unroll
@@ -97,18 +147,21 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
 #pragma unroll
         for (int d = 0; d < DIM; ++d) ut += ji[r * DIM + d] * vel[d];
         const double* dp = vdphi + (r * C::NQV + q) * C::NPP;
-        taxpy<NP, W>(dp, w * (s[0] * ut), acc, 0);
+        taxpy<NP, WH>(dp, w * (s[0] * ut), acc, 0);
 #pragma unroll
         for (int d = 0; d < DIM; ++d)
-          taxpy<NP, W>(dp, w * (s[1 + d] * ut + p * ji[r * DIM + d]), acc, (1 + d) * NP);
-        taxpy<NP, W>(dp, w * ((s[NEQ - 1] + p) * ut), acc, (NEQ - 1) * NP);
+          taxpy<NP, WH>(dp, w * (s[1 + d] * ut + p * ji[r * DIM + d]), acc, (1 + d) * NP);
+        taxpy<NP, WH>(dp, w * ((s[NEQ - 1] + p) * ut), acc, (NEQ - 1) * NP);
       }
     } else {
+      double Ft[DIM * NEQ];
+      Physics<PH, DIM, NEQ>::vflux(s, ji, P, Ft);
 #pragma unroll
       for (int r = 0; r < DIM; ++r) {
-        double a = ji[r * DIM + 0] * P.vel[0] + ji[r * DIM + 1] * P.vel[1];
-        if (DIM == 3) a += ji[r * DIM + 2] * P.vel[2];
-        taxpy<NP, W>(vdphi + (r * C::NQV + q) * C::NPP, w * (a * s[0]), acc, 0);
+        const double* dp = vdphi + (r * C::NQV + q) * C::NPP;
+#pragma unroll
+        for (int k = 0; k < NEQH; ++k)
+          if (mine && k < nown) taxpy<NP, WH>(dp, w * own_part<C>(Ft + r * NEQ, h, k), acc, k * NP);
       }
     }
   }
@@ -148,18 +201,21 @@ __device__ __forceinline__ TpeSide tpe_side(const View& v, int64_t s, int64_t en
   return t;
 }
 
-// Surface contribution of this lane's side, added into acc.  All lanes call.
+// Surface contribution of this lane (side, equation group), added into acc.
+// All lanes call (shuffles).
 template <class C, int PH>
-__device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, int side,
-                                            const double (&u)[Tpe<C>::W], const Params& P,
-                                            double (&acc)[Tpe<C>::W]) {
-  constexpr int W = Tpe<C>::W, NP = C::NP, NEQ = C::NEQ;
+__device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, int side, int h,
+                                            int nown, const double (&u)[Tpe<C>::WH],
+                                            const Params& P, double (&acc)[Tpe<C>::WH]) {
+  constexpr int NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH;
+  constexpr int H = Tpe<C>::H;
   const double* fphi = st + C::S_FPHI + t.mycode * (C::NQF * C::NPP);
   const double* fw = st + C::S_FW;
   const double sc = side ? t.scale : -t.scale;
+  const int eq0 = h * NEQH;
 #pragma unroll 1
   for (int g = 0; g < C::NQF; ++g) {
-    double own[NEQ], sL[NEQ], sR[NEQ], out[NEQ], row[C::NPP];
+    double row[C::NPP];
     {
       const double2* r2 = reinterpret_cast<const double2*>(fphi + g * C::NPP);
 #pragma unroll
@@ -169,19 +225,25 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
         row[2 * j + 1] = a.y;
       }
     }
+    double own[NEQH], s[NEQ], sL[NEQ], sR[NEQ], out[NEQ];
 #pragma unroll
-    for (int k = 0; k < NEQ; ++k) {
+    for (int k = 0; k < NEQH; ++k) {
       if (t.has) {
         double tr = 0.0;
 #pragma unroll
         for (int j = 0; j < NP; ++j) tr = fma(row[j], u[k * NP + j], tr);
         own[k] = tr;
-      } else {
-        own[k] = (t.valid && side) ? P.ff[k] : 0.0;   // far-field ghost
+      } else {  // far-field ghost state on physical boundaries
+        const int e = (eq0 + k < NEQ) ? eq0 + k : NEQ - 1;
+        own[k] = (t.valid && side) ? P.ff[e] : 0.0;
       }
-      const double other = __shfl_xor_sync(kFull, own[k], 1);
-      sL[k] = side ? other : own[k];
-      sR[k] = side ? own[k] : other;
+    }
+    assemble_state<C>(own, h, s);
+#pragma unroll
+    for (int k = 0; k < NEQ; ++k) {
+      const double other = __shfl_xor_sync(kFull, s[k], H);
+      sL[k] = side ? other : s[k];
+      sR[k] = side ? s[k] : other;
     }
     // canonical (single-domain) orientation for partitioner-flipped surfaces,
     // through ONE call site so the arithmetic is bit-identical to 1 domain
@@ -199,24 +261,22 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
     if (flip) c = -c;
     if (t.owner) {
 #pragma unroll
-      for (int k = 0; k < NEQ; ++k) {
-        const double f = c * out[k];
+      for (int k = 0; k < NEQH; ++k) {
+        if (k < nown) {
+          const double f = c * own_part<C>(out, h, k);
 #pragma unroll
-        for (int j = 0; j < NP; ++j) acc[k * NP + j] = fma(row[j], f, acc[k * NP + j]);
+          for (int j = 0; j < NP; ++j) acc[k * NP + j] = fma(row[j], f, acc[k * NP + j]);
+        }
       }
     }
   }
 }
 
-// Whole-block loads/stores.  Blocks are 32-byte aligned (stride padded to
-// 4 doubles), so W % 4 == 0 blocks move as 256-bit accesses
-// (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a): one full 32-byte sector per
-// lane per instruction, half the L1 wavefronts of 128-bit accesses.
 // 256-bit accesses (PTX v4.f64; ptxas emits LDG/STG.E.ENL2.256).  CUDA 12.9
 // gives double4 only 16-byte alignment, so the C++ type would split them.
 __device__ __forceinline__ void ld4_nc(const double* p, double& a, double& b, double& c, double& d) {
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 __device__ __forceinline__ void ld4(const double* p, double& a, double& b, double& c, double& d) {
   asm("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -227,53 +287,71 @@ __device__ __forceinline__ void st4(double* p, double a, double b, double c, dou
                : "memory");
 }
 
-template <int W>
-__device__ __forceinline__ void tload(const double* __restrict__ src, double (&dst)[W]) {
-  if constexpr (W % 4 == 0) {
+// This lane's run of `n` doubles (n <= N): the whole block when H = 1
+// (256-bit when N % 4 == 0), its equation group when H = 2 (128-bit pairs).
+template <int N, bool kWhole>
+__device__ __forceinline__ void tload(const double* __restrict__ src, int n, double (&dst)[N]) {
+  if constexpr (kWhole && N % 4 == 0) {
 #pragma unroll
-    for (int j = 0; j < W / 4; ++j)
+    for (int j = 0; j < N / 4; ++j)
       ld4_nc(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
-  } else {
+  } else if constexpr (N % 2 == 0) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-      const double2 a = __ldg(s2 + j);
-      dst[2 * j] = a.x;
-      dst[2 * j + 1] = a.y;
+    for (int j = 0; j < N / 2; ++j) {
+      if (kWhole || 2 * j < n) {
+        const double2 a = __ldg(s2 + j);
+        dst[2 * j] = a.x;
+        dst[2 * j + 1] = a.y;
+      } else {
+        dst[2 * j] = dst[2 * j + 1] = 0.0;
+      }
     }
-    if constexpr (W % 2) dst[W - 1] = __ldg(src + W - 1);
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) dst[j] = (kWhole || j < n) ? __ldg(src + j) : 0.0;
   }
 }
 
-template <int W>
-__device__ __forceinline__ void tload_rw(const double* src, double (&dst)[W]) {
-  if constexpr (W % 4 == 0) {
+template <int N, bool kWhole>
+__device__ __forceinline__ void tload_rw(const double* src, int n, double (&dst)[N]) {
+  if constexpr (kWhole && N % 4 == 0) {
 #pragma unroll
-    for (int j = 0; j < W / 4; ++j)
+    for (int j = 0; j < N / 4; ++j)
       ld4(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
-  } else {
+  } else if constexpr (N % 2 == 0) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-      const double2 a = s2[j];
-      dst[2 * j] = a.x;
-      dst[2 * j + 1] = a.y;
+    for (int j = 0; j < N / 2; ++j) {
+      if (kWhole || 2 * j < n) {
+        const double2 a = s2[j];
+        dst[2 * j] = a.x;
+        dst[2 * j + 1] = a.y;
+      } else {
+        dst[2 * j] = dst[2 * j + 1] = 0.0;
+      }
     }
-    if constexpr (W % 2) dst[W - 1] = src[W - 1];
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) dst[j] = (kWhole || j < n) ? src[j] : 0.0;
   }
 }
 
-template <int W>
-__device__ __forceinline__ void tstore(double* dst, const double (&src)[W]) {
-  if constexpr (W % 4 == 0) {
+template <int N, bool kWhole>
+__device__ __forceinline__ void tstore(double* dst, int n, const double (&src)[N]) {
+  if constexpr (kWhole && N % 4 == 0) {
 #pragma unroll
-    for (int j = 0; j < W / 4; ++j)
+    for (int j = 0; j < N / 4; ++j)
       st4(dst + 4 * j, src[4 * j], src[4 * j + 1], src[4 * j + 2], src[4 * j + 3]);
-  } else {
+  } else if constexpr (N % 2 == 0) {
     double2* d2 = reinterpret_cast<double2*>(dst);
 #pragma unroll
-    for (int j = 0; j < W / 2; ++j) d2[j] = make_double2(src[2 * j], src[2 * j + 1]);
-    if constexpr (W % 2) dst[W - 1] = src[W - 1];
+    for (int j = 0; j < N / 2; ++j)
+      if (kWhole || 2 * j < n) d2[j] = make_double2(src[2 * j], src[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (kWhole || j < n) dst[j] = src[j];
   }
 }
 
@@ -283,89 +361,86 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 }
 
 // ------------------------------------------------------------- kernels
-// L2 prefetch of a whole element block through the TMA engine (one
-// instruction per block; the data lands in L2 while the current tile
-// computes, so the next tile's loads hit L2 instead of waiting on HBM).
-__device__ __forceinline__ void prefetch_l2(const double* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+#ifndef MC_TPE_MINB_SURF
+#define MC_TPE_MINB_SURF 3
+#endif
+
+struct TpeLane {
+  int lane, side, h, grp, nown, eq0;
+};
+
+template <class C>
+__device__ __forceinline__ TpeLane tpe_lane() {
+  constexpr int H = Tpe<C>::H;
+  TpeLane L;
+  L.lane = threadIdx.x & 31;
+  L.grp = L.lane / (2 * H);
+  L.side = (L.lane / H) & 1;
+  L.h = L.lane % H;
+  L.eq0 = L.h * Tpe<C>::NEQH;
+  L.nown = (L.h == 0) ? Tpe<C>::NEQH : Tpe<C>::NEQ1;
+  return L;
 }
 
 // kVol: the color contains first touches (volume fused); kRK: the color
 // contains last touches of an RK stage (update fused).  The host picks the
 // variant per color launch so surface-only passes carry no volume code.
-#ifndef MC_TPE_GLOBAL_TABLES
-#define MC_TPE_GLOBAL_TABLES 0
-#endif
-#ifndef MC_TPE_MINB_SURF
-#define MC_TPE_MINB_SURF 3
-#endif
 template <class C, int PH, bool kRK, bool kVol>
-__global__ void __launch_bounds__(Tpe<C>::THREADS, kVol ? Tpe<C>::MINB : MC_TPE_MINB_SURF)
+__global__ void __launch_bounds__(Tpe<C>::THREADS,
+                                  (kVol || Tpe<C>::H == 2) ? Tpe<C>::MINB : MC_TPE_MINB_SURF)
 k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
               int64_t end) {
-  constexpr int W = Tpe<C>::W;
-#if MC_TPE_GLOBAL_TABLES
-  const double* st = v.ptables;          // 4-30 KB, stays L1/L2 resident
-#else
+  using T = Tpe<C>;
+  constexpr int WH = T::WH;
+  constexpr bool kWhole = T::H == 1;
   extern __shared__ double sts[];
   tpe_stage<C>(v.tables, sts);
   const double* st = sts;
-#endif
-  const int lane = threadIdx.x & 31, side = lane & 1;
+  const TpeLane ln = tpe_lane<C>();
+  const int n = ln.nown * C::NP;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
-#ifdef MC_TPE_PREFETCH
-  const uint32_t blk = uint32_t(v.stride * 8);
-#endif
-  for (int64_t tile = begin + warp * 16; tile < end; tile += nwarp * 16) {
-    const int64_t s = tile + (lane >> 1);
-#ifdef MC_TPE_PREFETCH
-    {  // prefetch the next tile of this warp into L2
-      const int64_t sn = s + nwarp * 16;
-      if (sn < end) {
-        const int en = side ? __ldg(v.right + sn) : __ldg(v.left + sn);
-        if (en >= 0) {
-          prefetch_l2(U + int64_t(en) * v.stride, blk);
-          if (!kVol && en < v.n_elements) prefetch_l2(R + int64_t(en) * v.stride, blk);
-          if (kRK && rk.a != 0.0 && en < v.n_elements) prefetch_l2(rk.U0 + int64_t(en) * v.stride, blk);
-        }
-      }
-    }
-#endif
-    const TpeSide t = tpe_side<C>(v, s, end, side);
-    const bool first = kVol && t.owner && (t.code & (side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
-    const bool last = kRK && t.owner && (t.code & (side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
-    const int64_t off = int64_t(t.has ? t.e : 0) * v.stride;
-    double u[W], acc[W];
-    if (t.has) tload<W>(U + off, u);
+  for (int64_t tile = begin + warp * T::SW; tile < end; tile += nwarp * T::SW) {
+    const int64_t s = tile + ln.grp;
+    const TpeSide t = tpe_side<C>(v, s, end, ln.side);
+    const bool first = kVol && t.owner && (t.code & (ln.side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
+    const bool last = kRK && t.owner && (t.code & (ln.side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
+    const int64_t off = int64_t(t.has ? t.e : 0) * v.stride + ln.eq0 * C::NP;
+    double u[WH], acc[WH];
+    if (t.has) tload<WH, kWhole>(U + off, n, u);
     else {
 #pragma unroll
-      for (int j = 0; j < W; ++j) u[j] = 0.0;
+      for (int j = 0; j < WH; ++j) u[j] = 0.0;
     }
-    if (t.owner && !first) tload_rw<W>(R + off, acc);
+    if (t.owner && !first) tload_rw<WH, kWhole>(R + off, n, acc);
     else {
 #pragma unroll
-      for (int j = 0; j < W; ++j) acc[j] = 0.0;
+      for (int j = 0; j < WH; ++j) acc[j] = 0.0;
     }
     if constexpr (kVol) {
-      if (first) tpe_volume<C, PH>(st, u, v.jinv + int64_t(t.e) * (C::DIM * C::DIM), v.prm, acc);
+      const double* jp = v.jinv + int64_t(first ? t.e : 0) * (C::DIM * C::DIM);
+      if constexpr (T::H == 1) {
+        if (first) tpe_volume<C, PH>(st, u, jp, 0, ln.nown, true, v.prm, acc);
+      } else if (__any_sync(kFull, first)) {   // the whole warp takes part in the shuffles
+        tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc);
+      }
     }
-    tpe_surface<C, PH>(st, t, side, u, v.prm, acc);
+    tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc);
     if (t.owner) {
       if (last) {
-        if (rk.save_u0) tstore<W>(rk.U0 + off, u);
+        if (rk.save_u0) tstore<WH, kWhole>(rk.U0 + off, n, u);
         if (rk.a != 0.0) {
-          double u0[W];
-          tload<W>(rk.U0 + off, u0);
+          double u0[WH];
+          tload<WH, kWhole>(rk.U0 + off, n, u0);
 #pragma unroll
-          for (int j = 0; j < W; ++j) acc[j] = rk.a * u0[j] + rk.b * fma(rk.dt, acc[j], u[j]);
+          for (int j = 0; j < WH; ++j) acc[j] = rk.a * u0[j] + rk.b * fma(rk.dt, acc[j], u[j]);
         } else {
 #pragma unroll
-          for (int j = 0; j < W; ++j) acc[j] = rk.b * fma(rk.dt, acc[j], u[j]);
+          for (int j = 0; j < WH; ++j) acc[j] = rk.b * fma(rk.dt, acc[j], u[j]);
         }
-        tstore<W>(U + off, acc);
+        tstore<WH, kWhole>(U + off, n, acc);
       } else {
-        tstore<W>(R + off, acc);
+        tstore<WH, kWhole>(R + off, n, acc);
       }
     }
   }
@@ -374,60 +449,79 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
 template <class C, int PH, bool kAtomic>
 __global__ void __launch_bounds__(Tpe<C>::THREADS, Tpe<C>::MINB)
 k_tpe_uncolored(View v, const double* __restrict__ U, double* __restrict__ out) {
-  constexpr int W = Tpe<C>::W;
+  using T = Tpe<C>;
+  constexpr int WH = T::WH;
+  constexpr bool kWhole = T::H == 1;
   extern __shared__ double st[];
   tpe_stage<C>(v.tables, st);
-  const int lane = threadIdx.x & 31, side = lane & 1;
+  const TpeLane ln = tpe_lane<C>();
+  const int n = ln.nown * C::NP;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t end = v.n_surfaces;
-  for (int64_t tile = warp * 16; tile < end; tile += nwarp * 16) {
-    const int64_t s = tile + (lane >> 1);
-    const TpeSide t = tpe_side<C>(v, s, end, side);
-    double u[W], acc[W];
-    if (t.has) tload<W>(U + int64_t(t.e) * v.stride, u);
+  for (int64_t tile = warp * T::SW; tile < end; tile += nwarp * T::SW) {
+    const int64_t s = tile + ln.grp;
+    const TpeSide t = tpe_side<C>(v, s, end, ln.side);
+    double u[WH], acc[WH];
+    if (t.has) tload<WH, kWhole>(U + int64_t(t.e) * v.stride + ln.eq0 * C::NP, n, u);
     else {
 #pragma unroll
-      for (int j = 0; j < W; ++j) u[j] = 0.0;
+      for (int j = 0; j < WH; ++j) u[j] = 0.0;
     }
 #pragma unroll
-    for (int j = 0; j < W; ++j) acc[j] = 0.0;
-    tpe_surface<C, PH>(st, t, side, u, v.prm, acc);
+    for (int j = 0; j < WH; ++j) acc[j] = 0.0;
+    tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc);
     if (kAtomic) {
       if (t.owner) {
-        double* dst = out + int64_t(t.e) * v.stride;
+        double* dst = out + int64_t(t.e) * v.stride + ln.eq0 * C::NP;
 #pragma unroll
-        for (int j = 0; j < W; ++j) atomicAdd(dst + j, acc[j]);
+        for (int j = 0; j < WH; ++j)
+          if (kWhole || j < n) atomicAdd(dst + j, acc[j]);
       }
     } else if (t.valid) {
       if (!t.owner) {
 #pragma unroll
-        for (int j = 0; j < W; ++j) acc[j] = 0.0;
+        for (int j = 0; j < WH; ++j) acc[j] = 0.0;
       }
-      tstore<W>(out + (2 * s + side) * v.stride, acc);
+      tstore<WH, kWhole>(out + (2 * s + ln.side) * v.stride + ln.eq0 * C::NP, n, acc);
     }
   }
 }
 
+// Volume integral for all owned elements (unfused strategies): H lanes per
+// element, 32/H elements per warp.
 template <class C, int PH>
 __global__ void __launch_bounds__(Tpe<C>::THREADS, Tpe<C>::MINB)
 k_tpe_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
-  constexpr int W = Tpe<C>::W;
+  using T = Tpe<C>;
+  constexpr int WH = T::WH, H = T::H;
+  constexpr bool kWhole = H == 1;
   extern __shared__ double st[];
   tpe_stage<C>(v.tables, st);
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < v.n_elements;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    double u[W], acc[W];
-    tload<W>(U + e * v.stride, u);
+  const int lane = threadIdx.x & 31, h = lane % H;
+  const int nown = (h == 0) ? T::NEQH : T::NEQ1, eq0 = h * T::NEQH, n = nown * C::NP;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t tile = warp * (32 / H); tile < v.n_elements; tile += nwarp * (32 / H)) {
+    const int64_t e = tile + lane / H;
+    const bool has = e < v.n_elements;
+    const int64_t off = (has ? e : 0) * v.stride + eq0 * C::NP;
+    double u[WH], acc[WH];
+    if (has) tload<WH, kWhole>(U + off, n, u);
+    else {
 #pragma unroll
-    for (int j = 0; j < W; ++j) acc[j] = 0.0;
-    tpe_volume<C, PH>(st, u, v.jinv + e * (C::DIM * C::DIM), v.prm, acc);
-    tstore<W>(R + e * v.stride, acc);
+      for (int j = 0; j < WH; ++j) u[j] = 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < WH; ++j) acc[j] = 0.0;
+    tpe_volume<C, PH>(st, u, v.jinv + (has ? e : 0) * (C::DIM * C::DIM), h, nown, has, v.prm,
+                      acc);
+    if (has) tstore<WH, kWhole>(R + off, n, acc);
   }
 }
 
 // Write the padded table layout (what tpe_stage puts in shared memory) to
-// global memory once per operator; kernels may read it through L1.
+// global memory once per operator (kept for experiments reading tables via L1).
 template <class C>
 __global__ void k_stage_global(const double* __restrict__ g, double* out) {
   extern __shared__ double sts[];
