@@ -62,7 +62,35 @@ def gauss_jacobi(n: int, alpha: float, beta: float = 0.0):
     return x, mu0 * V[0] ** 2
 
 
+def _symmetric_deg5(kind):
+    """Radon 7-point triangle / Walkington 14-point tetrahedron (degree 5)."""
+    if kind == "tri":
+        r = 15 ** 0.5
+        a, b, c, d = (6 - r) / 21, (9 + 2 * r) / 21, (6 + r) / 21, (9 - 2 * r) / 21
+        P = np.array([[1 / 3, 1 / 3], [a, a], [a, b], [b, a], [c, c], [c, d], [d, c]])
+        W = np.array([9 / 80] + [(155 - r) / 2400] * 3 + [(155 + r) / 2400] * 3)
+        return P, W
+    P, W = [], []
+    for v, wv in ((0.0927352503108912, 0.01224884051939366),
+                  (0.3108859192633006, 0.01878132095300264)):
+        for i in range(4):                          # (v, v, v, 1-3v) in barycentrics
+            lam = np.full(4, v)
+            lam[i] = 1 - 3 * v
+            P.append(lam[1:])
+            W.append(wv)
+    c, wc = 0.0455037041256496, 0.007091003462846911
+    for i in range(4):
+        for j in range(i + 1, 4):                   # (c, c, 1/2-c, 1/2-c)
+            lam = np.full(4, c)
+            lam[[i, j]] = 0.5 - c
+            P.append(lam[1:])
+            W.append(wc)
+    return np.array(P), np.array(W)
+
+
 def vol_rule(kind: str, p: int):
+    if p == 2 and kind in ("tri", "tet"):
+        return _symmetric_deg5(kind)
     n = p + 1
     a, wa = gauss_jacobi(n, 0.0)
     if kind == "quad":

@@ -47,8 +47,10 @@ struct Cfg {
   static constexpr int NP = (K == TRI) ? (P + 1) * (P + 2) / 2
                           : (K == QUAD) ? (P + 1) * (P + 1)
                                         : (P + 1) * (P + 2) * (P + 3) / 6;
-  static constexpr int NQF = (K == TET) ? (P + 1) * (P + 1) : P + 1;
-  static constexpr int NQV = (K == TET) ? (P + 1) * (P + 1) * (P + 1) : (P + 1) * (P + 1);
+  // quadrature (dg/basis.py): degree-5 symmetric rules for p = 2 on simplices
+  static constexpr int NQF = (K == TET) ? (P == 2 ? 7 : (P + 1) * (P + 1)) : P + 1;
+  static constexpr int NQV = (K == TET) ? (P == 2 ? 14 : (P + 1) * (P + 1) * (P + 1))
+                           : (K == TRI && P == 2) ? 7 : (P + 1) * (P + 1);
   static constexpr int NCODES = (K == QUAD || K == TET) ? 24 : 18;
 #ifdef MC_DG_DMMA
   static constexpr bool DMMA_ON = (K != TET);

@@ -22,7 +22,9 @@ a quadrature rule exact for its square.
 
 Quadrature: Gauss-Legendre on edges (p+1 points, weights summing to 1),
 collapsed Gauss-Jacobi on triangles/tetrahedra ((p+1)^d points) and the
-tensor Gauss-Legendre rule on quads.  Volume weights sum to the reference
+tensor Gauss-Legendre rule on quads; for p = 2 the minimal symmetric
+degree-5 rules replace the collapsed ones (7 points on triangles and tet
+faces, 14 in tetrahedra).  Volume weights sum to the reference
 measure (1/2, 1, 1/6); face weights sum to 1.
 """
 
@@ -189,8 +191,49 @@ def _gj(n, alpha):
     return np.asarray(x, dtype=np.float64), np.asarray(w, dtype=np.float64)
 
 
+# Minimal symmetric degree-5 rules used for p = 2 (exact to degree 2p+1 like
+# the collapsed rules they replace, with fewer points): Radon's 7-point
+# triangle rule and the 14-point tetrahedron rule (Walkington).  Their
+# exactness is verified in tests/test_dg_oracle.py.
+_S15 = np.sqrt(15.0)
+_RADON_A, _RADON_B = (6 - _S15) / 21, (9 + 2 * _S15) / 21
+_RADON_C, _RADON_D = (6 + _S15) / 21, (9 - 2 * _S15) / 21
+TET14 = ((0.0927352503108912, 0.01224884051939366),
+         (0.3108859192633006, 0.01878132095300264),
+         (0.0455037041256496, 0.007091003462846911))
+
+
+def _radon7():
+    pts = np.array([[1 / 3, 1 / 3], [_RADON_A, _RADON_A], [_RADON_A, _RADON_B],
+                    [_RADON_B, _RADON_A], [_RADON_C, _RADON_C], [_RADON_C, _RADON_D],
+                    [_RADON_D, _RADON_C]])
+    w = np.array([9 / 80] + [(155 - _S15) / 2400] * 3 + [(155 + _S15) / 2400] * 3)
+    return pts, w
+
+
+def _tet14():
+    pts, w = [], []
+    for v, wv in TET14[:2]:
+        for i in range(4):
+            bc = [v] * 4
+            bc[i] = 1 - 3 * v
+            pts.append(bc[1:])
+            w.append(wv)
+    c, wc = TET14[2]
+    for i, j in itertools.combinations(range(4), 2):
+        bc = [c] * 4
+        bc[i] = bc[j] = 0.5 - c
+        pts.append(bc[1:])
+        w.append(wc)
+    return np.array(pts), np.array(w)
+
+
 def volume_rule(kind: ElementKind, p: int):
     """(points (nq, dim), weights (nq,)) on the reference element."""
+    if p == 2 and kind is ElementKind.TRIANGLE:
+        return _radon7()
+    if p == 2 and kind is ElementKind.TET:
+        return _tet14()
     n = p + 1
     if kind is ElementKind.QUAD:
         t, w = gauss_legendre01(n)

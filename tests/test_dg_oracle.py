@@ -81,3 +81,26 @@ def test_advection_converges_at_p_plus_one(kind, p):
         errs.append(np.sqrt(np.sum(np.abs(c["det"])[:, None, None] * e ** 2)) / n)
     rate = np.log2(errs[0] / errs[1])
     assert rate > p + 0.6, (errs, rate)
+
+
+@pytest.mark.parametrize("kind,p", [("tri", 1), ("tri", 2), ("tri", 3), ("quad", 2), ("tet", 1),
+                                    ("tet", 2), ("tet", 3)])
+def test_quadrature_exactness(kind, p):
+    """Volume rules integrate every monomial up to degree 2p+1 exactly; the
+    product and the oracle implement the same rules."""
+    from math import factorial
+    from paper_1601_07613_b200.dg.basis import volume_rule
+    X, W = D.vol_rule(kind, p)
+    Xp, Wp = volume_rule(KINDS[kind], p)
+    assert np.allclose(X, Xp, atol=1e-15) and np.allclose(W, Wp, atol=1e-15)
+    dim = X.shape[1]
+    import itertools
+    for e in itertools.product(range(2 * p + 2), repeat=dim):
+        if sum(e) > 2 * p + 1:
+            continue
+        num = np.sum(W * np.prod(X ** np.array(e), axis=1))
+        if kind == "quad":
+            exact = np.prod([1.0 / (k + 1) for k in e])
+        else:
+            exact = np.prod([factorial(k) for k in e]) / factorial(sum(e) + dim)
+        assert abs(num - exact) < 1e-14, (e, num, exact)
