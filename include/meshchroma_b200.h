@@ -47,6 +47,7 @@ extern "C" {
 #define MC_ECUDA 7         /* CUDA runtime failure                         */
 #define MC_ENOMEM 8        /* allocation failure                           */
 #define MC_EUNSUPPORTED 9  /* configuration without a compiled kernel      */
+#define MC_ENONMANIFOLD 10 /* NonManifoldError (errors.py; mesh.py:283-290) */
 
 const char* mc_last_error(void);
 /* 1000*major + 10*minor of the library; lets bindings check the ABI. */
@@ -217,6 +218,27 @@ int mc_dg_ssprk3(mc_dg* dg, double* U_dev, double* work_dev, double dt,
                  int n_steps, void* stream);
 /* End-to-end: copy U from host, n_steps SSP-RK3 steps, copy back. */
 int mc_dg_ssprk3_host(mc_dg* dg, double* U_host, double dt, int n_steps);
+
+/* ------------------------------------------------------------------ */
+/* Surface extraction (mesh.assemble, reference mesh.py:207-300)       */
+/* ------------------------------------------------------------------ */
+/* Side slots sorted by packed vertex key on the GPU (CUB radix sort),
+ * surfaces numbered by first encounter in element-major slot order, left =
+ * smaller element id.  Inputs are HOST arrays already validated by the
+ * caller (kind codes 0..2, vertex ids in range, no repeated vertices).
+ * Returns MC_ENONMANIFOLD (handle still valid: fetch surf_count to report)
+ * when a surface has more than two elements, MC_EUNSUPPORTED when the
+ * packed key does not fit 64 bits. */
+typedef struct mc_assembly mc_assembly;
+int mc_assemble_create(int64_t n_elements, int64_t n_vertices, const int8_t* kind_codes,
+                       const int64_t* elem_verts /* n_elements x 4 */, int width,
+                       mc_assembly** out, int64_t* n_surfaces);
+/* host outputs (any may be NULL): surf_verts n_surfaces x width (sorted
+ * tuples), surf_elems n_surfaces x 2, elem_surfs n_elements x 4 (-1 pad),
+ * surf_count n_surfaces (elements per surface) */
+int mc_assemble_result(mc_assembly* a, int64_t* surf_verts, int64_t* surf_elems,
+                       int64_t* elem_surfs, int32_t* surf_count);
+int mc_assemble_destroy(mc_assembly* a);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libmeshchroma_b200.so"
 
 MC_OK, MC_EINVAL, MC_ECONFLICT, MC_ESWAPBUDGET, MC_ERESTARTS = 0, 1, 2, 3, 4
 MC_EAUDIT, MC_EINTERNAL, MC_ECUDA, MC_ENOMEM, MC_EUNSUPPORTED = 5, 6, 7, 8, 9
+MC_ENONMANIFOLD = 10
 
 _STATUS_TO_EXC = {
     MC_EINVAL: ValueError,
@@ -31,6 +32,7 @@ _STATUS_TO_EXC = {
     MC_ECUDA: errors.NativeLibraryError,
     MC_ENOMEM: MemoryError,
     MC_EUNSUPPORTED: NotImplementedError,
+    MC_ENONMANIFOLD: errors.NonManifoldError,
 }
 
 
@@ -96,6 +98,10 @@ _SIGS = {
                                    C.c_double, C.c_double, _P]),
     "mc_dg_ssprk3": (C.c_int, [_P, _P, _P, C.c_double, C.c_int, _P]),
     "mc_dg_ssprk3_host": (C.c_int, [_P, _P, C.c_double, C.c_int]),
+    "mc_assemble_create": (C.c_int, [_I64, _I64, _P, _P, C.c_int, C.POINTER(_P),
+                                     C.POINTER(_I64)]),
+    "mc_assemble_result": (C.c_int, [_P, _P, _P, _P, _P]),
+    "mc_assemble_destroy": (C.c_int, [_P]),
 }
 
 EXPORTED = tuple(_SIGS)

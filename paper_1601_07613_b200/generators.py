@@ -89,7 +89,7 @@ def _cell_corners(table, nx, ny):
     return i, j, a, b, c, d
 
 
-def gen_tri_rect(nx: int, ny: int, periodic=False) -> Mesh:
+def gen_tri_rect(nx: int, ny: int, periodic=False, *, device=None) -> Mesh:
     """Two right triangles per unit cell, diagonal alternating with parity."""
     px, py = _pair(periodic)
     _check_axis("nx", nx, px)
@@ -106,10 +106,10 @@ def gen_tri_rect(nx: int, ny: int, periodic=False) -> Mesh:
     ev[:, 1, 2] = d
     ev = ev.reshape(-1, MAX_ELEM_VERTS)
     kinds = np.full(len(ev), KIND_TO_CODE[ElementKind.TRIANGLE], np.int8)
-    return assemble(coords, kinds, ev)
+    return assemble(coords, kinds, ev, device=device)
 
 
-def gen_quad_rect(nx: int, ny: int, periodic=False) -> Mesh:
+def gen_quad_rect(nx: int, ny: int, periodic=False, *, device=None) -> Mesh:
     """One unit quad per cell, counter-clockwise (a, b, c, d)."""
     px, py = _pair(periodic)
     _check_axis("nx", nx, px)
@@ -118,7 +118,7 @@ def gen_quad_rect(nx: int, ny: int, periodic=False) -> Mesh:
     _, _, a, b, c, d = _cell_corners(table, nx, ny)
     ev = np.stack([a, b, c, d], axis=1).astype(np.int64)
     kinds = np.full(len(ev), KIND_TO_CODE[ElementKind.QUAD], np.int8)
-    return assemble(coords, kinds, ev)
+    return assemble(coords, kinds, ev, device=device)
 
 
 # six tetrahedra per hex cell sharing the v0-v7 diagonal; corner k of the
@@ -128,7 +128,7 @@ _HEX_SPLIT = np.array([(0, 1, 3, 7), (0, 1, 7, 5), (0, 5, 7, 4),
                       dtype=np.int64)
 
 
-def gen_tet_prism(nx: int, ny: int, nz: int) -> Mesh:
+def gen_tet_prism(nx: int, ny: int, nz: int, *, device=None) -> Mesh:
     """Box of unit hex cells, each cut into six positively oriented tets."""
     for name, n in (("nx", nx), ("ny", ny), ("nz", nz)):
         _check_axis(name, n, False)
@@ -148,11 +148,11 @@ def gen_tet_prism(nx: int, ny: int, nz: int) -> Mesh:
     ev[:, :, :] = corner[:, _HEX_SPLIT]
     ev = ev.reshape(-1, MAX_ELEM_VERTS)
     kinds = np.full(len(ev), KIND_TO_CODE[ElementKind.TET], np.int8)
-    return assemble(coords, kinds, ev)
+    return assemble(coords, kinds, ev, device=device)
 
 
-def shuffle_elements(mesh: Mesh, seed: int) -> Mesh:
+def shuffle_elements(mesh: Mesh, seed: int, *, device=None) -> Mesh:
     """Re-assemble with element ids permuted by numpy's PCG64 stream."""
     order = np.random.default_rng(seed).permutation(mesh.n_elements)
     return assemble(mesh.vertices, mesh.elem_kind[order],
-                    mesh.elem_verts[order])
+                    mesh.elem_verts[order], device=device)

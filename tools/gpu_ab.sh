@@ -3,7 +3,6 @@ run() {  # $1 = defines, $2 = env assignment
   env $2 python bench.py --no-cpu --e2e-steps 1 > gpurun_out/ab.json 2>&1
   python -c "import json,sys; d=json.load(open('gpurun_out/ab.json')); print('[$1 | $2]', round(d['value']/1e9,3), 'G edges/s', round(d['ms_per_step'],3), 'ms', round(d['roofline']['frac'],3), {k: round(v) for k,v in d['roofline']['per_color_gbs'].items()})" || tail -3 gpurun_out/ab.json
 }
-run "MC_VOL_UNROLL=1" "X=1"
-run "MC_VOL_UNROLL=3" "X=1"
-run "MC_VOL_UNROLL=9" "X=1"
-run "MC_VOL_UNROLL=3 MC_MINB_TPE=2" "X=1"
+run "" "X=1"
+run "MC_MINB_TPE=4" "X=1"
+run "MC_MINB_TPE=5" "X=1"
