@@ -240,6 +240,22 @@ int mc_assemble_result(mc_assembly* a, int64_t* surf_verts, int64_t* surf_elems,
                        int64_t* elem_surfs, int32_t* surf_count);
 int mc_assemble_destroy(mc_assembly* a);
 
+/* ------------------------------------------------------------------ */
+/* AMR split-edge color propagation (amr._materialize classification,  */
+/* reference amr.py:221-245 + :158-164)                                */
+/* ------------------------------------------------------------------ */
+/* Host arrays in and out.  fine_surf_verts: n_fine_surfaces x 2 sorted
+ * (midpoint vertex ids are n_base_vertices + index into split); split: the
+ * base edges that were split, ascending.  Outputs per fine surface: origin
+ * (0 whole, 1 half, 2 interior), related base edge, half index (1/2, else
+ * 0) and the 6-palette color.  MC_EINTERNAL (AssertionError) when a fine
+ * edge has no base counterpart. */
+int mc_amr_classify(int64_t n_fine_surfaces, const int64_t* fine_surf_verts,
+                    int64_t n_base_vertices, int64_t n_split, const int64_t* split,
+                    int64_t n_base_surfaces, const int64_t* base_surf_verts,
+                    const int32_t* base_colors, int8_t* surf_origin, int64_t* base_surface,
+                    int8_t* half_index, int32_t* colors);
+
 #ifdef __cplusplus
 }
 #endif

@@ -102,6 +102,7 @@ _SIGS = {
                                      C.POINTER(_I64)]),
     "mc_assemble_result": (C.c_int, [_P, _P, _P, _P, _P]),
     "mc_assemble_destroy": (C.c_int, [_P]),
+    "mc_amr_classify": (C.c_int, [_I64, _P, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -42,7 +42,11 @@ struct Tpe {
 #else
   // tets keep the group kernel: with 27 volume points the 2x redundant flux
   // of H = 2 loses to the task scheme (measured)
+#ifdef MC_TPE_TET
+  static constexpr bool OK = H == 1 || (H == 2 && PAIRS);
+#else
   static constexpr bool OK = H == 1 || (H == 2 && PAIRS && C::DIM == 2);
+#endif
 #endif
   static constexpr int SW = 16 / (H ? H : 1);                      // surfaces per warp
   static constexpr int THREADS = 128;

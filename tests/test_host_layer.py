@@ -174,3 +174,20 @@ def test_amr_errors():
     rec, rec_col = P.reconstruct_refinement(ref.mesh, ref.parents, fine)
     assert rec.map.refined == ref.map.refined
     assert np.array_equal(rec_col.colors, fine.colors)
+
+
+def test_family_table_worked_example():
+    """reference test_amr.py:59-72 (single triangle, colors by edge)."""
+    mesh = P.build_surfaces([(0, 0), (1, 0), (0, 1)], [("tri", (0, 1, 2))])
+    by_verts = {(0, 1): 2, (1, 2): 1, (0, 2): 3}
+    colors = np.array([by_verts[tuple(int(v) for v in mesh.surf_verts[k])]
+                       for k in range(mesh.n_surfaces)], dtype=np.int32)
+    ref, fine = P.refine(mesh, P.SurfaceColoring(colors, 3), [0])
+    assert ref.mesh.n_elements == 4 and ref.mesh.n_surfaces == 9
+    fam = ref.map.families[0]
+    assert fam == ref.map.family(0) == tuple(ref.map.families)[0]
+    assert fam.parent_edge_colors == (2, 1, 3)
+    assert fam.child_edge_colors == ((2, 5), (1, 4), (3, 6))
+    assert fam.interior_edge_colors == (3, 2, 1)
+    assert fam.children == (0, 1, 2, 3)
+    assert len(ref.map.families) == 1 and ref.map.families == (fam,)

@@ -3,4 +3,5 @@ run() {  # $1 = defines, $2 = env assignment
   env $2 python bench.py --no-cpu --e2e-steps 1 ${BENCH_ARGS} > gpurun_out/ab.json 2>&1
   python -c "import json,sys; d=json.load(open('gpurun_out/ab.json')); print('[$1 | $2]', round(d['value']/1e9,3), 'G edges/s', round(d['ms_per_step'],3), 'ms', round(d['roofline']['frac'],3), {k: round(v) for k,v in d['roofline']['per_color_gbs'].items()})" || tail -3 gpurun_out/ab.json
 }
-for e in "X=1" "MC_NO_PIPE=1" "X=1"; do run "" "$e"; done
+export BENCH_ARGS="--config c4"
+for d in "" "MC_TPE_TET" "MC_TPE_TET MC_MINB_TPE=3"; do run "$d" "X=1"; done
