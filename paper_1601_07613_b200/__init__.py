@@ -28,6 +28,8 @@ from .generators import (FAMILIES, GeneratorSpec, gen_quad_rect, gen_tet_prism,
 from .mesh import (ConnectivityGraph, Diagnostic, Element, ElementKind, Mesh,
                    Surface, assemble, build_surfaces, connectivity_graph,
                    validate, vizing_bound)
+from .meshio import (NativeMesh, read_msh, read_native, write_native,
+                     write_report)
 from .reorder import (CoalescingReport, ReorderingPlan, apply_plan, build_plan,
                       coalescing_metric, invert_plan)
 from .sweeps import (AccumulationState, MemoryEstimate, assert_race_free,
