@@ -4,4 +4,4 @@ run() {  # $1 = defines, $2 = env assignment
   python -c "import json,sys; d=json.load(open('gpurun_out/ab.json')); print('[$1 | $2]', round(d['value']/1e9,3), 'G edges/s', round(d['ms_per_step'],3), 'ms', round(d['roofline']['frac'],3), {k: round(v) for k,v in d['roofline']['per_color_gbs'].items()})" || tail -3 gpurun_out/ab.json
 }
 export BENCH_ARGS="--config c4"
-for d in "" "MC_TPE_TET" "MC_TPE_TET MC_MINB_TPE=3"; do run "$d" "X=1"; done
+for e in "X=1" "MC_GROUP_KERNEL=1"; do run "" "$e"; done
