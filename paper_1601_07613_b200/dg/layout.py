@@ -186,13 +186,18 @@ def _normals(kind, Xl, local_l, surf_pts_l, centroid):
 
 
 def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
-                       period=None, mortars=None, owned=None, flipped=None) -> SurfaceList:
+                       period=None, mortars=None, owned=None, flipped=None,
+                       code_sort=False) -> SurfaceList:
     """Assemble the device surface list from a color-grouped mesh.
 
     ``colors`` must be non-decreasing over surface ids (a mesh produced by
     apply_plan).  ``mortars``: optional (n, 3) hanging triples
     (full, half_lo, half_hi) in this mesh's surface ids.  ``owned``:
     number of owned elements (elements >= owned are read-only ghosts).
+    ``code_sort``: within each color, order surfaces by their (left, right)
+    side codes (stable), so the lanes of a warp read the same reference-face
+    table rows (shared-memory broadcasts).  Any order within a color is
+    race free and leaves every element's accumulation order unchanged.
     """
     kind = mesh_kind(mesh)
     dim = DIM[kind]
@@ -310,6 +315,12 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
         code |= np.where(np.asarray(flipped)[sid], FLAG_FLIPPED, 0)
     if (L >= ne).any():
         raise ValueError("left elements must be owned")
+
+    if code_sort:
+        perm = np.lexsort((np.arange(len(sid)), code & 0xFFF, col))
+        L, R, code, geom, col, sid = L[perm], R[perm], code[perm], geom[perm], col[perm], sid[perm]
+        has_r, ghost_r, loc_l, loc_r = has_r[perm], ghost_r[perm], loc_l[perm], loc_r[perm]
+        mortar_r = mortar_r[perm]
 
     bounds = np.zeros(n_colors + 1, dtype=np.int64)
     bounds[1:] = np.cumsum(np.bincount(col, minlength=n_colors + 1)[1:n_colors + 1])
