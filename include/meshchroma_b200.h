@@ -17,6 +17,10 @@
  *   mc_sweep_buffered_i64[_host]     -> sweeps.sweep_buffered :179-204
  *   mc_sweep_atomic_i64              -> (absent in the reference: SPEC.md:411;
  *                                        paper §1 "atomic operations")
+ *   mc_assemble_create/_result       -> mesh.assemble :207-300 (surface ids,
+ *                                        incidence, NonManifoldError :275-283)
+ *   mc_amr_classify                  -> amr._materialize :221-245 + colors
+ *                                        :158-164 (split-edge propagation)
  *   mc_dg_*                          -> Algorithm 1 / Eq. (2) of the paper
  *                                        (PAPER.md:29-33, 64-82); the
  *                                        reference implements only the
