@@ -204,8 +204,41 @@ def peaks():
 
 
 # ---------------------------------------------------------------- CPU leg
-def cpu_sample(spec, steps=1):
-    """Oracle (numpy fp64) SSP-RK3 on the bounded sample; edges/s."""
+_CPU_PROBLEM = {}
+
+
+def blas_threads() -> int:
+    """Threads numpy's BLAS may use (the oracle's einsum/matmul work)."""
+    try:
+        from threadpoolctl import threadpool_info
+        n = [int(i.get("num_threads", 1)) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:  # noqa: BLE001
+        return 1
+
+
+def cpu_sample(spec, steps=1, min_seconds=0.0):
+    """Oracle (numpy fp64) SSP-RK3 on the bounded sample mesh; edges/s.
+    The sample problem is built once per process (setup is not timed); with
+    ``min_seconds`` the step count grows until the timed work lasts that long."""
+    key = spec["desc"]
+    if key not in _CPU_PROBLEM:
+        _CPU_PROBLEM[key] = _cpu_problem(spec)
+    prob, U0, ne, ns = _CPU_PROBLEM[key]
+    from oracle import dg_oracle as D
+    total, done, t_all = 0, 0, 0.0
+    while True:
+        U = U0.copy()
+        t0 = time.perf_counter()
+        D.ssprk3(prob, U, 1e-3, steps)
+        t_all += time.perf_counter() - t0
+        done += steps
+        if t_all >= min_seconds:
+            break
+    return 3 * done * ns / t_all, t_all, ne, ns, done
+
+
+def _cpu_problem(spec):
     import paper_1601_07613_b200 as P
     from oracle import dg_oracle as D
     from paper_1601_07613_b200.dg.operator import default_freestream
@@ -235,11 +268,7 @@ def cpu_sample(spec, steps=1):
     U = np.zeros((mesh.n_elements, neq, nb))
     ff = np.asarray(phys.farfield) if spec["physics"] == "euler" else np.ones(1)
     U[:, :, 0] = ff[None, :] * (1.0 / D.Basis(kind, spec["p"]).scale[0])
-    t0 = time.perf_counter()
-    D.ssprk3(prob, U, 1e-3, steps)
-    dt = time.perf_counter() - t0
-    ns = int(active.sum())
-    return 3 * steps * ns / dt, dt, mesh.n_elements, ns
+    return prob, U, mesh.n_elements, int(active.sum())
 
 
 def run_reference(args):
@@ -253,19 +282,21 @@ def run_reference(args):
         cpu_sample(spec, 1)
     rates, times = [], []
     for _ in range(args.steps):
-        r, t, ne, ns = cpu_sample(spec, 1)
+        r, t, ne, ns, _n = cpu_sample(spec, 1)
         rates.append(r)
         times.append(t)
     value = float(np.median(rates))
+    threads = blas_threads()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * float(np.median(times)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": spec["desc"], "sample_elements": ne, "sample_surfaces": ns},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"oracle/dg_oracle.py SSP-RK3 step on a {ne}-element, "
-                                   f"{ns}-surface mesh of the same family"},
+                                   f"{ns}-surface mesh of the same family (numpy; BLAS "
+                                   f"threads {threads})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -416,10 +447,12 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        r, t, sne, sns = cpu_sample(spec, 1)
-        cpu = {"value": r, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"oracle/dg_oracle.py numpy fp64 SSP-RK3 step, {sne} elements / "
-                         f"{sns} surfaces of the same mesh family ({t:.1f} s)"}
+        r, t, sne, sns, nsteps = cpu_sample(spec, 1, min_seconds=10.0)
+        threads = blas_threads()
+        cpu = {"value": r, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"oracle/dg_oracle.py numpy fp64, {nsteps} SSP-RK3 steps on "
+                         f"{sne} elements / {sns} surfaces of the same mesh family "
+                         f"({t:.1f} s; BLAS threads {threads})"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -501,6 +534,22 @@ def variants(op, U_host, spec, stream, reps=5):
         ms = timeit(fn)
         out[f"{name}_ms"] = ms
         out[f"{name}_edges_per_s"] = op.n_surfaces / (ms * 1e-3)
+    # CPU integer-mode baseline beside it: the oracle's numpy
+    # restatement of the reference's sweep_sequential (sweeps.py:74-86), and a
+    # check that the GPU colored totals equal it bit for bit
+    from oracle import sweeps_oracle as SO
+    se = op.layout_mesh.surf_elems
+    pay_h = P.default_payload(op.n_surfaces)
+    t0 = time.perf_counter()
+    ref_tot = SO.sweep_sequential(se, op.n_elements, pay_h)
+    cpu_s = time.perf_counter() - t0
+    lay.sweep_colored(pay, tot, stream)
+    torch.cuda.synchronize()
+    out["cpu_int_sequential"] = {"kind": "port", "cores": 1, "seconds": cpu_s,
+                                 "edges_per_s": op.n_surfaces / cpu_s,
+                                 "sample": "oracle/sweeps_oracle.sweep_sequential (numpy "
+                                           "np.add.at), full mesh"}
+    out["int_colored_equals_cpu"] = bool(np.array_equal(tot.cpu().numpy(), ref_tot))
     return out
 
 

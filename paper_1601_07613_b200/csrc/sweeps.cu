@@ -55,6 +55,7 @@ struct mc_layout {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kU = 4;   // surfaces per thread per iteration in k_sweep_color
 
 inline int grid_for(int64_t n, int threads = kThreads) {
   int64_t g = (n + threads - 1) / threads;
@@ -68,13 +69,30 @@ k_sweep_color(const int2* __restrict__ lr, const int32_t* __restrict__ sid,
               const int64_t* __restrict__ payload, int64_t* totals,
               int64_t begin, int64_t end) {
   // one color: no two surfaces share an element, so plain read-modify-write
-  // is race free; that is the whole point of the coloring.
-  for (int64_t k = begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-       k < end; k += int64_t(gridDim.x) * blockDim.x) {
-    const int2 e = __ldg(&lr[k]);
-    const int64_t v = __ldg(&payload[kIdentity ? k : __ldg(&sid[k])]);
-    totals[e.x] += v;
-    if (e.y >= 0) totals[e.y] -= v;
+  // is race free; that is the whole point of the coloring.  kU surfaces per
+  // thread (stride = grid) with every load issued before the first store, so
+  // the read-modify-write latency is paid once per kU surfaces.
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t k0 = begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k0 < end;
+       k0 += kU * stride) {
+    int2 e[kU];
+    int64_t v[kU], tl[kU], tr[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t k = k0 + u * stride;
+      e[u] = k < end ? __ldg(&lr[k]) : make_int2(-1, -1);
+      v[u] = k < end ? __ldg(&payload[kIdentity ? k : __ldg(&sid[k])]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      tl[u] = e[u].x >= 0 ? totals[e[u].x] : 0;
+      tr[u] = e[u].y >= 0 ? totals[e[u].y] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (e[u].x >= 0) totals[e[u].x] = tl[u] + v[u];
+      if (e[u].y >= 0) totals[e[u].y] = tr[u] - v[u];
+    }
   }
 }
 
@@ -331,9 +349,9 @@ MC_API int mc_sweep_colored_i64(mc_layout* L, const int64_t* payload, int64_t* t
     const int64_t b = L->bounds[c - 1], e = L->bounds[c];
     if (e == b) continue;
     if (L->identity)
-      k_sweep_color<true><<<grid_for(e - b), kThreads, 0, s>>>(L->d_lr, L->d_sid, payload, totals, b, e);
+      k_sweep_color<true><<<grid_for((e - b + kU - 1) / kU), kThreads, 0, s>>>(L->d_lr, L->d_sid, payload, totals, b, e);
     else
-      k_sweep_color<false><<<grid_for(e - b), kThreads, 0, s>>>(L->d_lr, L->d_sid, payload, totals, b, e);
+      k_sweep_color<false><<<grid_for((e - b + kU - 1) / kU), kThreads, 0, s>>>(L->d_lr, L->d_sid, payload, totals, b, e);
   }
   return check_launch();
 }
