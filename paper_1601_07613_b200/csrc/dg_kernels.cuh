@@ -275,11 +275,58 @@ struct Physics<ADV, DIM, NEQ> {
   }
 };
 
+// fp64 reciprocal and square root for the flux: the hardware approximation
+// (MUFU.RCP64H / MUFU.RSQ64H) refined by Newton steps to full double
+// precision (within an ulp or two of the IEEE result), without the
+// special-case slow path of the IEEE division / square root.  Densities and
+// pressures are positive and normal here; MC_IEEE_DIV restores the IEEE
+// operations.
+#ifdef MC_IEEE_DIV
+constexpr bool kFluxFastMath = false;
+#else
+constexpr bool kFluxFastMath = true;
+#endif
+
+template <bool kFast = true>
+__device__ __forceinline__ double flux_rcp(double x) {
+  if constexpr (!(kFast && kFluxFastMath)) {
+    return 1.0 / x;
+  } else {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+  }
+}
+
+template <bool kFast = true>
+__device__ __forceinline__ double flux_sqrt(double x) {
+  if constexpr (!(kFast && kFluxFastMath)) {
+    return sqrt(x);
+  } else {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    // y <- y (3 - x y^2) / 2, twice; then sqrt = x y with one Heron correction
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    const double s0 = x * y;
+    return fma(fma(-s0, s0, x), 0.5 * y, s0);
+  }
+}
+
 template <int DIM, int NEQ>
 struct Physics<EULER, DIM, NEQ> {
+  // measured: the Newton forms win in the 2D register kernels (c2 +1 %,
+  // c3 +2 %) and lose in the 3D group kernel (c4 -5 %, register pressure)
+  static constexpr bool kFast = DIM == 2;
   __device__ static __forceinline__ void prim(const double* s, const Params& P, double* u,
-                                              double& p) {
-    const double inv = 1.0 / s[0];
+                                              double& p, double& inv) {
+    inv = flux_rcp<kFast>(s[0]);
     double ke = 0.0;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
@@ -291,17 +338,19 @@ struct Physics<EULER, DIM, NEQ> {
 
   __device__ static __forceinline__ void lf(const double* sL, const double* sR, const double* n,
                                             const Params& P, double* out) {
-    double uL[DIM], uR[DIM], pL, pR;
-    prim(sL, P, uL, pL);
-    prim(sR, P, uR, pR);
+    double uL[DIM], uR[DIM], pL, pR, iL, iR;
+    prim(sL, P, uL, pL, iL);
+    prim(sR, P, uR, pR, iR);
     double vnL = 0.0, vnR = 0.0;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       vnL += uL[d] * n[d];
       vnR += uR[d] * n[d];
     }
-    const double cL = sqrt(P.gamma * pL / sL[0]);
-    const double cR = sqrt(P.gamma * pR / sR[0]);
+    // sound speeds from the reciprocal density prim() already formed (one
+    // fp64 division per state instead of two)
+    const double cL = flux_sqrt<kFast>(P.gamma * pL * iL);
+    const double cR = flux_sqrt<kFast>(P.gamma * pR * iR);
     const double lam = fmax(fabs(vnL) + cL, fabs(vnR) + cR);
     // F.n = s*vn + p*(0, n, vn)
     out[0] = 0.5 * (sL[0] * vnL + sR[0] * vnR) - 0.5 * lam * (sR[0] - sL[0]);
@@ -315,8 +364,8 @@ struct Physics<EULER, DIM, NEQ> {
 
   __device__ static __forceinline__ void vflux(const double* s, const double* ji,
                                                const Params& P, double* Ft) {
-    double u[DIM], p;
-    prim(s, P, u, p);
+    double u[DIM], p, inv;
+    prim(s, P, u, p, inv);
 #pragma unroll
     for (int r = 0; r < DIM; ++r) {
       double ut = 0.0;
