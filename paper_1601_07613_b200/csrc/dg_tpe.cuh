@@ -206,7 +206,14 @@ __device__ __forceinline__ TpeSide tpe_side(const View& v, int64_t s, int64_t en
 }
 
 // Surface contribution of this lane (side, equation group), added into acc.
-// All lanes call (shuffles).
+// All lanes call (shuffles).  Each side evaluates the flux OUT of its own
+// element, F_own = lf(own state, other state, own outward normal): no
+// left/right selects per point, and the arithmetic of a lane depends only
+// on its own element's view of the surface, so a partitioner-flipped
+// surface (MC_FLAG_FLIPPED) gives the owned element bit-identical
+// contributions without special handling.  The two sides' values are
+// negatives of each other up to rounding (the oracle's single flux times
+// -/+1 agrees to ~1e-16 relative).
 template <class C, int PH>
 __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, int side, int h,
                                             int nown, const double (&u)[Tpe<C>::WH],
@@ -215,8 +222,11 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
   constexpr int H = Tpe<C>::H;
   const double* fphi = st + C::S_FPHI + t.mycode * (C::NQF * C::NPP);
   const double* fw = st + C::S_FW;
-  const double sc = side ? t.scale : -t.scale;
+  const double sc = -t.scale;
   const int eq0 = h * NEQH;
+  double nO[C::DIM];
+#pragma unroll
+  for (int d = 0; d < C::DIM; ++d) nO[d] = side ? -t.n[d] : t.n[d];
 #pragma unroll 1
   for (int g = 0; g < C::NQF; ++g) {
     double row[C::NPP];
@@ -229,7 +239,7 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
         row[2 * j + 1] = a.y;
       }
     }
-    double own[NEQH], s[NEQ], sL[NEQ], sR[NEQ], out[NEQ];
+    double own[NEQH], s[NEQ], x[NEQ], out[NEQ];
 #pragma unroll
     for (int k = 0; k < NEQH; ++k) {
       if (t.has) {
@@ -239,31 +249,15 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
         own[k] = tr;
       } else {  // far-field ghost state on physical boundaries
         const int e = (eq0 + k < NEQ) ? eq0 + k : NEQ - 1;
-        own[k] = (t.valid && side) ? P.ff[e] : 0.0;
+        own[k] = (t.valid && side) ? P.ff[e] : 1.0;
       }
     }
     assemble_state<C>(own, h, s);
 #pragma unroll
-    for (int k = 0; k < NEQ; ++k) {
-      const double other = __shfl_xor_sync(kFull, s[k], H);
-      sL[k] = side ? other : s[k];
-      sR[k] = side ? s[k] : other;
-    }
-    // canonical (single-domain) orientation for partitioner-flipped surfaces,
-    // through ONE call site so the arithmetic is bit-identical to 1 domain
-    const bool flip = (t.code & MC_FLAG_FLIPPED) != 0;
-    double cL[NEQ], cR[NEQ], nn[C::DIM];
-#pragma unroll
-    for (int k = 0; k < NEQ; ++k) {
-      cL[k] = flip ? sR[k] : sL[k];
-      cR[k] = flip ? sL[k] : sR[k];
-    }
-#pragma unroll
-    for (int d = 0; d < C::DIM; ++d) nn[d] = flip ? -t.n[d] : t.n[d];
-    Physics<PH, C::DIM, NEQ>::lf(cL, cR, nn, P, out);
-    double c = sc * fw[g];
-    if (flip) c = -c;
+    for (int k = 0; k < NEQ; ++k) x[k] = __shfl_xor_sync(kFull, s[k], H);
+    Physics<PH, C::DIM, NEQ>::lf(s, x, nO, P, out);
     if (t.owner) {
+      const double c = sc * fw[g];
 #pragma unroll
       for (int k = 0; k < NEQH; ++k) {
         if (k < nown) {

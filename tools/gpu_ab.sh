@@ -3,9 +3,8 @@ run() {  # $1 = defines, $2 = env assignment
   env $2 python bench.py --no-cpu --e2e-steps 1 ${BENCH_ARGS} > gpurun_out/ab.json 2>&1
   python -c "import json,sys; d=json.load(open('gpurun_out/ab.json')); print('[$1 | $2 | ${BENCH_ARGS}]', round(d['value']/1e9,3), 'G edges/s', round(d['ms_per_step'],3), 'ms', round(d['roofline']['frac'],3), {k: round(v) for k,v in d['roofline']['per_color_gbs'].items()})" || tail -3 gpurun_out/ab.json
 }
-./tools/flux_math_probe
-python -m pytest tests/test_dg_gpu.py tests/test_partition_gpu.py tests/test_convergence_gpu.py -x -q 2>&1 | tail -2
-for cfg in c2 c4; do
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for cfg in c2 c3 c5; do
   export BENCH_ARGS="--config $cfg"
   run "" "X=1"
 done
