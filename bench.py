@@ -380,7 +380,10 @@ def main():
         total_ms = float(t.item())
     ms_per_step = total_ms / max(args.steps, 1)
     ns, ne = op.n_surfaces, op.n_elements
-    ns_global, ne_global = op.mesh.n_surfaces, op.mesh.n_elements
+    # surfaces evaluated per RHS: the DG surface list (AMR: coarse full edges
+    # are replaced by their two mortar halves); partitioned: the global mesh
+    ns_global = op.n_surfaces if world == 1 else op.mesh.n_surfaces
+    ne_global = op.mesh.n_elements
     value = 3 * ns_global / (ms_per_step * 1e-3)
     dof_rate = ne_global * op.n_basis * op.n_equations * 3 / (ms_per_step * 1e-3)
 
@@ -525,28 +528,29 @@ def variants(op, U_host, spec, stream, reps=5):
     out["buffer_gb_truncated"] = mem.gb_truncated
     # integer Algorithm 1 on the reordered mesh
     lay = DeviceLayout(op.layout_mesh, op.layout_coloring)
-    pay = torch.from_numpy(P.default_payload(op.n_surfaces)).cuda()
-    tot = torch.zeros(op.n_elements, dtype=torch.int64, device="cuda")
-    buf = torch.zeros(2 * op.n_surfaces, dtype=torch.int64, device="cuda")
+    nsm = op.layout_mesh.n_surfaces        # mesh surfaces (AMR: incl. coarse full edges)
+    pay = torch.from_numpy(P.default_payload(nsm)).cuda()
+    tot = torch.zeros(op.layout_mesh.n_elements, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(2 * nsm, dtype=torch.int64, device="cuda")
     for name, fn in (("int_colored", lambda: lay.sweep_colored(pay, tot, stream)),
                      ("int_buffered", lambda: lay.sweep_buffered(pay, buf, tot, stream)),
                      ("int_atomic", lambda: lay.sweep_atomic(pay, tot, stream))):
         ms = timeit(fn)
         out[f"{name}_ms"] = ms
-        out[f"{name}_edges_per_s"] = op.n_surfaces / (ms * 1e-3)
+        out[f"{name}_edges_per_s"] = nsm / (ms * 1e-3)
     # CPU integer-mode baseline beside it: the oracle's numpy
     # restatement of the reference's sweep_sequential (sweeps.py:74-86), and a
     # check that the GPU colored totals equal it bit for bit
     from oracle import sweeps_oracle as SO
     se = op.layout_mesh.surf_elems
-    pay_h = P.default_payload(op.n_surfaces)
+    pay_h = P.default_payload(nsm)
     t0 = time.perf_counter()
-    ref_tot = SO.sweep_sequential(se, op.n_elements, pay_h)
+    ref_tot = SO.sweep_sequential(se, op.layout_mesh.n_elements, pay_h)
     cpu_s = time.perf_counter() - t0
     lay.sweep_colored(pay, tot, stream)
     torch.cuda.synchronize()
     out["cpu_int_sequential"] = {"kind": "port", "cores": 1, "seconds": cpu_s,
-                                 "edges_per_s": op.n_surfaces / cpu_s,
+                                 "edges_per_s": nsm / cpu_s,
                                  "sample": "oracle/sweeps_oracle.sweep_sequential (numpy "
                                            "np.add.at), full mesh"}
     out["int_colored_equals_cpu"] = bool(np.array_equal(tot.cpu().numpy(), ref_tot))
