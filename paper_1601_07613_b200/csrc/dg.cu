@@ -29,6 +29,12 @@ struct mc_dg {
   double* d_buffer = nullptr;      // 2*ns blocks (buffered strategy)
   double* d_host_U = nullptr;      // host path scratch: U, U0, R
   cudaStream_t stream = nullptr;
+  // one SSP-RK3 step captured as a CUDA graph (9-12 launches replayed with
+  // one cudaGraphLaunch), keyed by the arguments baked into it
+  cudaGraphExec_t step_exec = nullptr;
+  double *g_U = nullptr, *g_work = nullptr;
+  double g_dt = 0.0;
+  cudaStream_t g_stream = nullptr;
 };
 
 namespace {
@@ -201,6 +207,7 @@ MC_API int mc_dg_destroy(mc_dg* h) {
   cudaFree(h->d_slots);
   cudaFree(h->d_buffer);
   cudaFree(h->d_host_U);
+  if (h->step_exec) cudaGraphExecDestroy(h->step_exec);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return MC_OK;
@@ -264,15 +271,58 @@ MC_API int mc_dg_ssprk3(mc_dg* h, double* U, double* work, double dt, int n_step
   cudaStream_t s = as_stream(stream);
   double* U0 = work;
   double* R = work + (h->ne + h->ng) * h->stride;
-  for (int step = 0; step < n_steps; ++step) {
+  auto one_step = [&]() -> int {
     // stage 1 saves U0 := U in its last-touch pass (no separate copy)
     mcdg::RK r1{U0, 0.0, 1.0, dt, 1};
     if (int rc = colored_pass(h, U, R, &r1, s)) return rc;
     mcdg::RK r2{U0, 0.75, 0.25, dt, 0};
     if (int rc = colored_pass(h, U, R, &r2, s)) return rc;
     mcdg::RK r3{U0, 1.0 / 3.0, 2.0 / 3.0, dt, 0};
-    if (int rc = colored_pass(h, U, R, &r3, s)) return rc;
+    return colored_pass(h, U, R, &r3, s);
+  };
+  // CUDA graph of one step on a non-default stream (capture is not allowed
+  // on the legacy stream); MC_NO_GRAPH=1 launches kernel by kernel
+  static const bool no_graph = std::getenv("MC_NO_GRAPH") != nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const bool graphable = !no_graph && s != nullptr && n_steps > 0 &&
+                         cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
+                         cap == cudaStreamCaptureStatusNone;
+  if (!graphable) {
+    for (int step = 0; step < n_steps; ++step)
+      if (int rc = one_step()) return rc;
+    return MC_OK;
   }
+  if (!h->step_exec || h->g_U != U || h->g_work != work || h->g_dt != dt || h->g_stream != s) {
+    cudaGraph_t g = nullptr;
+    DG_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int rc = one_step();
+    const cudaError_t ec = cudaStreamEndCapture(s, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ec != cudaSuccess) return mc_fail(MC_ECUDA, std::string("step capture: ") + cudaGetErrorString(ec));
+    if (h->step_exec) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(h->step_exec, g, &info) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphExecDestroy(h->step_exec);
+        h->step_exec = nullptr;
+      }
+    }
+    cudaError_t ei = cudaSuccess;
+    if (!h->step_exec) ei = cudaGraphInstantiate(&h->step_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {
+      h->step_exec = nullptr;
+      return mc_fail(MC_ECUDA, std::string("step graph: ") + cudaGetErrorString(ei));
+    }
+    h->g_U = U;
+    h->g_work = work;
+    h->g_dt = dt;
+    h->g_stream = s;
+  }
+  for (int step = 0; step < n_steps; ++step) DG_TRY(cudaGraphLaunch(h->step_exec, s));
   return MC_OK;
 }
 
