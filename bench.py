@@ -344,15 +344,27 @@ def main():
     stream = torch.cuda.current_stream()
     nc = op.n_colors
 
+    def mark(events, mode, a, c):
+        if events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            events.append((mode, a, c, ev))
+
     def step(events=None):
         for mode, a, b in STAGES:
-            if op.halo is not None:
-                op.halo.exchange(U)          # NCCL ghost exchange before each stage
-            for c in range(1, nc + 1):
-                if events is not None:
-                    ev = torch.cuda.Event(enable_timing=True)
-                    ev.record(stream)
-                    events.append((mode, a, c, ev))
+            if op.halo is None:
+                for c in range(1, nc + 1):
+                    mark(events, mode, a, c)
+                    op.color_pass_device(c, U, U0, R, mode, a, b, dt, stream)
+                continue
+            # NCCL ghost exchange overlapped with the ghost-free part of color 1
+            h = op.halo.start(U)
+            mark(events, mode, a, 1)
+            op.color_pass_device(1, U, U0, R, mode, a, b, dt, stream, part="inner")
+            op.halo.finish(U, h)
+            op.color_pass_device(1, U, U0, R, mode, a, b, dt, stream, part="interface")
+            for c in range(2, nc + 1):
+                mark(events, mode, a, c)
                 op.color_pass_device(c, U, U0, R, mode, a, b, dt, stream)
 
     def barrier():

@@ -217,6 +217,13 @@ int mc_dg_rk_stage(mc_dg* dg, double* U_dev, const double* U0_dev,
 int mc_dg_color_pass(mc_dg* dg, int color, double* U_dev, double* U0_dev,
                      double* R_dev, int rk_mode, double a, double b, double dt,
                      void* stream);
+/* As mc_dg_color_pass over surfaces [begin, end) of the color's list
+ * (relative to the color's first surface).  A partitioned layout puts the
+ * surfaces that touch ghost elements last in every color, so the interior
+ * part of the first color can run while the ghost exchange is in flight. */
+int mc_dg_color_range_pass(mc_dg* dg, int color, int64_t begin, int64_t end,
+                           double* U_dev, double* U0_dev, double* R_dev, int rk_mode,
+                           double a, double b, double dt, void* stream);
 /* n_steps SSP-RK3 steps; work_dev = 2 blocks arrays (U0, R scratch). */
 int mc_dg_ssprk3(mc_dg* dg, double* U_dev, double* work_dev, double dt,
                  int n_steps, void* stream);

@@ -96,6 +96,8 @@ _SIGS = {
                                  C.c_double, _P]),
     "mc_dg_color_pass": (C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int, C.c_double,
                                    C.c_double, C.c_double, _P]),
+    "mc_dg_color_range_pass": (C.c_int, [_P, C.c_int, _I64, _I64, _P, _P, _P, C.c_int,
+                                         C.c_double, C.c_double, C.c_double, _P]),
     "mc_dg_ssprk3": (C.c_int, [_P, _P, _P, C.c_double, C.c_int, _P]),
     "mc_dg_ssprk3_host": (C.c_int, [_P, _P, C.c_double, C.c_int]),
     "mc_assemble_create": (C.c_int, [_I64, _I64, _P, _P, C.c_int, C.POINTER(_P),

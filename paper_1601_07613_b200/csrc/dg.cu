@@ -246,11 +246,14 @@ MC_API int mc_dg_rk_stage(mc_dg* h, double* U, const double* U0, double* R, doub
   return colored_pass(h, U, R, &rk, as_stream(stream));
 }
 
-MC_API int mc_dg_color_pass(mc_dg* h, int color, double* U, double* U0, double* R, int rk_mode,
-                            double a, double b, double dt, void* stream) {
+MC_API int mc_dg_color_range_pass(mc_dg* h, int color, int64_t begin, int64_t end, double* U,
+                                  double* U0, double* R, int rk_mode, double a, double b,
+                                  double dt, void* stream) {
   if (!h || !U || !R) return mc_fail(MC_EINVAL, "null argument");
   if (color < 1 || color > h->n_colors) return mc_fail(MC_EINVAL, "bad color");
-  const int64_t bb = h->bounds[color - 1], e = h->bounds[color];
+  const int64_t c0 = h->bounds[color - 1], c1 = h->bounds[color];
+  if (begin < 0 || end < begin || c0 + end > c1) return mc_fail(MC_EINVAL, "bad surface range");
+  const int64_t bb = c0 + begin, e = c0 + end;
   if (e == bb) return MC_OK;
   const int grid = colored_grid(h, e - bb);
   if (rk_mode == 0) {
@@ -263,6 +266,14 @@ MC_API int mc_dg_color_pass(mc_dg* h, int color, double* U, double* U0, double* 
                            h->has_first[color], h->has_last[color]));
   }
   return MC_OK;
+}
+
+MC_API int mc_dg_color_pass(mc_dg* h, int color, double* U, double* U0, double* R, int rk_mode,
+                            double a, double b, double dt, void* stream) {
+  if (!h) return mc_fail(MC_EINVAL, "null argument");
+  if (color < 1 || color > h->n_colors) return mc_fail(MC_EINVAL, "bad color");
+  return mc_dg_color_range_pass(h, color, 0, h->bounds[color] - h->bounds[color - 1], U, U0, R,
+                                rk_mode, a, b, dt, stream);
 }
 
 MC_API int mc_dg_ssprk3(mc_dg* h, double* U, double* work, double dt, int n_steps,

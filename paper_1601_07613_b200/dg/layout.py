@@ -156,6 +156,7 @@ class SurfaceList:
     slot_ptr: np.ndarray      # (ne+1,) CSR of (2*s+side) slots per element
     slots: np.ndarray         # int32
     mesh_surface: np.ndarray  # source surface id (in the layout mesh) per entry
+    inner: np.ndarray | None = None   # per color: surfaces before the ghost-touching ones
 
     @property
     def n_surfaces(self) -> int:
@@ -316,14 +317,18 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
     if (L >= ne).any():
         raise ValueError("left elements must be owned")
 
-    if code_sort:
-        perm = np.lexsort((np.arange(len(sid)), code & 0xFFF, col))
+    if code_sort or (owned is not None and ghost_r.any()):
+        # partitioned: surfaces touching a ghost go last in their color, so
+        # the rest of the first color can run while the ghosts are exchanged
+        key2 = (code & 0xFFF) if code_sort else np.zeros(len(sid), dtype=np.int64)
+        perm = np.lexsort((np.arange(len(sid)), key2, ghost_r.astype(np.int64), col))
         L, R, code, geom, col, sid = L[perm], R[perm], code[perm], geom[perm], col[perm], sid[perm]
         has_r, ghost_r, loc_l, loc_r = has_r[perm], ghost_r[perm], loc_l[perm], loc_r[perm]
         mortar_r = mortar_r[perm]
 
     bounds = np.zeros(n_colors + 1, dtype=np.int64)
     bounds[1:] = np.cumsum(np.bincount(col, minlength=n_colors + 1)[1:n_colors + 1])
+    inner = np.bincount(col[~ghost_r], minlength=n_colors + 1)[1:n_colors + 1].astype(np.int64)
 
     # CSR of buffer slots per owned element (local side order for conforming
     # sides, mortar halves appended) for the buffer-and-reduce variant
@@ -342,4 +347,4 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
         left=L.astype(np.int32), right=np.where(has_r, R, -1).astype(np.int32),
         code=code.astype(np.uint32), geom=np.ascontiguousarray(geom),
         jinv=np.ascontiguousarray(jinv), detj=detj, slot_ptr=ptr,
-        slots=slot.astype(np.int32), mesh_surface=sid)
+        slots=slot.astype(np.int32), mesh_surface=sid, inner=inner)

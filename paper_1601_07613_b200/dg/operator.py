@@ -246,10 +246,40 @@ class DGOperator:
             float(a), float(b), float(dt), _native.stream_ptr(stream)))
 
     def color_pass_device(self, color: int, U_dev, U0_dev, R_dev, rk_mode: int = 0,
-                          a: float = 0.0, b: float = 1.0, dt: float = 0.0, stream=None) -> None:
-        _native.check(self._lib.mc_dg_color_pass(
-            self._h, int(color), _native.ptr(U_dev), _native.ptr(U0_dev), _native.ptr(R_dev),
-            int(rk_mode), float(a), float(b), float(dt), _native.stream_ptr(stream)))
+                          a: float = 0.0, b: float = 1.0, dt: float = 0.0, stream=None,
+                          part: str | None = None) -> None:
+        """One color launch.  ``part``: None = the whole color, "inner" =
+        the surfaces that touch no ghost element, "interface" = the rest
+        (a partitioned layout orders each color inner-first)."""
+        if part is None:
+            _native.check(self._lib.mc_dg_color_pass(
+                self._h, int(color), _native.ptr(U_dev), _native.ptr(U0_dev), _native.ptr(R_dev),
+                int(rk_mode), float(a), float(b), float(dt), _native.stream_ptr(stream)))
+            return
+        sl = self.surfaces
+        n = int(sl.bounds[color] - sl.bounds[color - 1])
+        k = int(sl.inner[color - 1])
+        lo, hi = (0, k) if part == "inner" else (k, n)
+        if part not in ("inner", "interface"):
+            raise ValueError(f"unknown part {part!r}")
+        _native.check(self._lib.mc_dg_color_range_pass(
+            self._h, int(color), lo, hi, _native.ptr(U_dev), _native.ptr(U0_dev),
+            _native.ptr(R_dev), int(rk_mode), float(a), float(b), float(dt),
+            _native.stream_ptr(stream)))
+
+    def stage_distributed(self, U_dev, U0_dev, R_dev, mode: int, a: float, b: float, dt: float,
+                          stream=None) -> None:
+        """One SSP-RK stage on a partitioned operator with the ghost exchange
+        overlapped: post the exchange, run the part of color 1 that touches
+        no ghost, complete the exchange, then the rest of color 1 and the
+        other colors."""
+        h = self.halo.start(U_dev) if self.halo is not None else None
+        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, stream, part="inner")
+        if h is not None:
+            self.halo.finish(U_dev, h)
+        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, stream, part="interface")
+        for c in range(2, self.n_colors + 1):
+            self.color_pass_device(c, U_dev, U0_dev, R_dev, mode, a, b, dt, stream)
 
     def work_device(self):
         import torch
@@ -258,16 +288,14 @@ class DGOperator:
     STAGES = ((2, 0.0, 1.0), (1, 0.75, 0.25), (1, 1.0 / 3.0, 2.0 / 3.0))
 
     def ssprk3_distributed(self, U_dev, work_dev, dt: float, steps: int = 1, stream=None) -> None:
-        """SSP-RK3 on a partitioned operator: ghost exchange before every
-        stage, then the stage's color launches (volume fused into first
-        touch, update into last touch, U0 saved in stage 1)."""
+        """SSP-RK3 on a partitioned operator: every stage exchanges the ghost
+        rows, overlapped with the ghost-free part of color 1
+        (``stage_distributed``); volume fused into first touch, update into
+        last touch, U0 saved in stage 1."""
         U0, R = work_dev[0], work_dev[1]
         for _ in range(steps):
             for mode, a, b in self.STAGES:
-                if self.halo is not None:
-                    self.halo.exchange(U_dev)
-                for c in range(1, self.n_colors + 1):
-                    self.color_pass_device(c, U_dev, U0, R, mode, a, b, dt, stream)
+                self.stage_distributed(U_dev, U0, R, mode, a, b, dt, stream)
 
     def ssprk3_device(self, U_dev, work_dev, dt: float, steps: int = 1, stream=None) -> None:
         _native.check(self._lib.mc_dg_ssprk3(self._h, _native.ptr(U_dev), _native.ptr(work_dev),

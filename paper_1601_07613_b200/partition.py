@@ -123,7 +123,10 @@ class HaloExchange:
         self.send_idx = {q: torch.as_tensor(ix, dtype=torch.int64, device=device)
                          for q, ix in part.send.items()}
 
-    def exchange(self, U) -> None:
+    def start(self, U):
+        """Gather the owned interface rows and post all sends / receives;
+        returns a handle for ``finish``.  With NCCL nothing blocks the host:
+        the transfers run on NCCL's stream, ordered after the gather."""
         import torch
         import torch.distributed as dist
         ops, bufs = [], []
@@ -136,8 +139,17 @@ class HaloExchange:
             buf = torch.empty((b - a,) + tuple(U.shape[1:]), dtype=U.dtype, device=U.device)
             recv.append((a, b, buf))
             ops.append(dist.P2POp(dist.irecv, buf, q))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, recv, bufs
+
+    def finish(self, U, handle) -> None:
+        """Wait for the transfers (the current stream waits, not the host,
+        with NCCL) and write the ghost rows."""
+        reqs, recv, _bufs = handle
+        for req in reqs:
+            req.wait()
         for a, b, buf in recv:
             U[a:b] = buf
+
+    def exchange(self, U) -> None:
+        self.finish(U, self.start(U))

@@ -73,6 +73,30 @@ def test_partition_invariants(world):
     assert ((seen == 2) == (interior & cut)).all() and (seen >= 1).all()
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_local_layout_orders_ghost_surfaces_last(world):
+    """Every color of a rank's device layout lists the surfaces that touch
+    no ghost first (``inner``), so that part of color 1 can run while the
+    ghost exchange is in flight; flags and CSR stay consistent."""
+    from paper_1601_07613_b200.dg.layout import FLAG_R_GHOST, build_surface_list
+    lm, lc = layout_case()
+    owner = slab_owner(lm, world)
+    for r in range(world):
+        part = build_partition(lm, lc.colors, lc.n_colors, owner, r)
+        sl = build_surface_list(part.mesh, part.colors, lc.n_colors, owned=part.n_owned,
+                                flipped=part.flipped)
+        assert sl.inner.sum() + (sl.code & FLAG_R_GHOST > 0).sum() == sl.n_surfaces
+        for c in range(lc.n_colors):
+            seg = (sl.code[sl.bounds[c]:sl.bounds[c + 1]] & FLAG_R_GHOST) > 0
+            k = int(sl.inner[c])
+            assert not seg[:k].any() and seg[k:].all()
+            assert (sl.right[sl.bounds[c]:sl.bounds[c] + k] < part.n_owned).all()
+        # the reordered list is still a race-free coloring of the local mesh
+        se = np.stack([sl.left, sl.right], 1).astype(np.int64)
+        col = np.repeat(np.arange(1, lc.n_colors + 1), np.diff(sl.bounds))
+        assert sweeps_oracle.first_race(se, col, lc.n_colors) is None
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

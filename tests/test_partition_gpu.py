@@ -8,6 +8,7 @@ import pytest
 
 import paper_1601_07613_b200 as P
 from paper_1601_07613_b200.dg import DGOperator
+from paper_1601_07613_b200.dg.layout import FLAG_R_GHOST
 
 pytestmark = pytest.mark.gpu
 
@@ -17,6 +18,18 @@ def emulated_exchange(ops, Us):
         for q, (a, b) in op.part.recv.items():
             src = ops[q].part.send[r]
             Us[r][a:b] = Us[q][src].to(Us[r].device)
+
+
+def emulated_gather(ops, Us):
+    """What every rank sends at the start of a stage (HaloExchange.start)."""
+    return {(q, r): Us[q][ops[q].part.send[r]].clone()
+            for r, op in enumerate(ops) for q in op.part.recv}
+
+
+def emulated_scatter(ops, Us, sent):
+    for r, op in enumerate(ops):
+        for q, (a, b) in op.part.recv.items():
+            Us[r][a:b] = sent[(q, r)]
 
 
 @pytest.mark.parametrize("world,kind", [(2, "tri"), (3, "tri"), (2, "tet"), (2, "quad")])
@@ -49,3 +62,43 @@ def test_partitioned_steps_match_single_domain(cuda, world, kind):
     bad = np.flatnonzero(np.abs(got - want).reshape(len(got), -1).max(axis=1) > 0)
     assert np.array_equal(got, want), (np.abs(got - want).max(), len(bad), len(got),
                                        np.abs(want).max())
+
+
+@pytest.mark.parametrize("world,kind", [(2, "tri"), (3, "tri"), (2, "tet")])
+def test_overlapped_exchange_matches_single_domain(cuda, world, kind):
+    """The stage order of ``stage_distributed`` (exchange posted, ghost-free
+    part of color 1, exchange completed, the rest): still bit-identical."""
+    import torch
+    mesh = {"tri": lambda: P.shuffle_elements(P.gen_tri_rect(14, 11), 3),
+            "tet": lambda: P.gen_tet_prism(4, 3, 2)}[kind]()
+    col, _ = P.color(mesh)
+    single = DGOperator(mesh, col, degree=2, physics="euler")
+    U = single.initial_state("wave")
+    dt = single.stable_dt(0.2)
+    want = single.ssprk3(U, dt, 2)
+    ops = [DGOperator(mesh, col, degree=2, physics="euler", world=world, rank=r)
+           for r in range(world)]
+    for op in ops:   # every color ordered ghost-free first
+        sl = op.surfaces
+        for c in range(op.n_colors):
+            seg = sl.code[sl.bounds[c]:sl.bounds[c + 1]] & FLAG_R_GHOST
+            k = int(sl.inner[c])
+            assert not seg[:k].any() and seg[k:].all()
+    Us = [torch.from_numpy(op.to_internal(U)).cuda() for op in ops]
+    works = [op.work_device() for op in ops]
+    for _ in range(2):
+        for mode, a, b in DGOperator.STAGES:
+            sent = emulated_gather(ops, Us)
+            for op, Ud, w in zip(ops, Us, works):
+                op.color_pass_device(1, Ud, w[0], w[1], mode, a, b, dt, part="inner")
+            emulated_scatter(ops, Us, sent)
+            for op, Ud, w in zip(ops, Us, works):
+                op.color_pass_device(1, Ud, w[0], w[1], mode, a, b, dt, part="interface")
+                for c in range(2, op.n_colors + 1):
+                    op.color_pass_device(c, Ud, w[0], w[1], mode, a, b, dt)
+    torch.cuda.synchronize()
+    got = np.empty_like(want)
+    for op, Ud in zip(ops, Us):
+        rows = Ud[: op.n_elements, : op.block_width()].cpu().numpy()
+        got[op.owned_user_ids()] = rows.reshape(op.n_elements, op.n_equations, op.n_basis)
+    assert np.array_equal(got, want), np.abs(got - want).max()

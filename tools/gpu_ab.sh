@@ -4,6 +4,6 @@ run() {  # $1 = defines, $2 = env assignment
   python -c "import json,sys; d=json.load(open('gpurun_out/ab.json')); print('[$1 | $2 | ${BENCH_ARGS}]', round(d['value']/1e9,3), 'G edges/s', round(d['ms_per_step'],3), 'ms', 'e2e', round(d['e2e']['value']/1e9,3), round(d['roofline']['frac'],3))" >> gpurun_out/ab_summary.txt 2>&1 || tail -3 gpurun_out/ab.json >> gpurun_out/ab_summary.txt
 }
 rm -f gpurun_out/ab_summary.txt
-python -m pytest tests/test_dg_gpu.py tests/test_partition_gpu.py -x -q 2>&1 | tail -2 >> gpurun_out/ab_summary.txt
-for cfg in c1 c2; do export BENCH_ARGS="--config $cfg"; for e in "X=1" "MC_NO_GRAPH=1"; do run "" "$e"; done; done
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2 >> gpurun_out/ab_summary.txt
+for cfg in c2; do export BENCH_ARGS="--config $cfg"; for e in "X=1"; do run "" "$e"; done; done
 cat gpurun_out/ab_summary.txt
