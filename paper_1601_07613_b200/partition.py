@@ -10,11 +10,14 @@ The reference has no partitioning; this module is new.
   elements after them; local surfaces = global surfaces with an owned
   element, kept in global color-major order (the restricted coloring stays
   valid); interface surfaces whose left element is remote are flipped so
-  the owned element is left (the LF flux is exactly antisymmetric under
-  the flip, so owned residuals are bit-identical to the single domain).
+  the owned element is left and marked; the kernels evaluate every side's
+  flux from its own element's view (register kernels) or in the original
+  orientation (group kernel), so owned residuals are bit-identical to the
+  single domain.
 * ``HaloExchange`` — ghost blocks in, owned interface blocks out, with
   ``torch.distributed`` point-to-point ops (NCCL on B200s, gloo in tests),
-  grouped in one ``batch_isend_irecv`` per stage.
+  grouped in one ``batch_isend_irecv`` per stage; ``start``/``finish`` let
+  the ghost-free part of the first color run while it is in flight.
 """
 
 from __future__ import annotations
