@@ -170,6 +170,7 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   if (e == cudaSuccess) e = cudaMalloc(&h->d_ptables, sizeof(double) * size_t(ops->stable_size));
   if (e == cudaSuccess) e = ops->stage_global(h->d_tables, h->d_ptables, nullptr);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = ops->upload_const(h->d_ptables);
   if (e != cudaSuccess) {
     mc_dg_destroy(h);
     return mc_fail(MC_ECUDA, std::string("DG table staging: ") + cudaGetErrorString(e));

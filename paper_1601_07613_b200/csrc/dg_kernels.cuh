@@ -42,6 +42,7 @@ enum Phys { ADV = 0, EULER = 1 };
 
 template <int K, int PH, int P>
 struct Cfg {
+  static constexpr int KIND = K, PDEG = P;
   static constexpr int DIM = (K == TET) ? 3 : 2;
   static constexpr int NEQ = (PH == ADV) ? 1 : DIM + 2;
   static constexpr int NP = (K == TRI) ? (P + 1) * (P + 2) / 2
@@ -145,6 +146,33 @@ struct Cfg {
   static constexpr int V_SIZE = V_FLAG + (EPW + 1) / 2 + 1;
   static constexpr int VSMEM = (S_TOTAL + WARPS * V_SIZE) * 8;
 };
+
+// Volume tables (basis values, reference gradients, weights at the volume
+// points) in constant memory, same padded layout as the shared-memory copy
+// from S_VPHI on.  Every lane of a warp reads the same entry at the same
+// time (uniform index), so these become uniform-datapath loads (LDCU) that
+// cost no shared-memory wavefronts.  One array per configuration; filled by
+// Instance::upload_const at operator creation.  Used by the one-lane-per-
+// element-side register kernel (c2: 3.43 -> 3.53 G edges/s); the group and
+// two-lane kernels keep the shared-memory copy (slower from constant memory:
+// c4 0.92 -> 0.82, c3 0.94 -> 0.92).  MC_SMEM_VOLTAB forces shared memory.
+template <int K, int P>
+__constant__ double c_voltab[Cfg<K, ADV, P>::S_SIZE - Cfg<K, ADV, P>::S_VPHI];
+
+template <class C, bool kConst>
+__device__ __forceinline__ const double* vol_tables(const double* st) {
+#ifdef MC_SMEM_VOLTAB
+  constexpr bool use = false;
+#else
+  constexpr bool use = kConst;
+#endif
+  if constexpr (use) {
+    (void)st;
+    return c_voltab<C::KIND, C::PDEG>;
+  } else {
+    return st + C::S_VPHI;
+  }
+}
 
 struct Params {
   double gamma;
@@ -429,9 +457,11 @@ __device__ __forceinline__ void volume_tasks(const double* st, double* vs, doubl
                                              const double (&u)[C::NP], int slot, int eq,
                                              bool mine, int lane, const Params& prm,
                                              double (&acc)[C::NP]) {
-  const double* vphi = st + C::S_VPHI;
-  const double* vdphi = st + C::S_VDPHI;
-  const double* vw = st + C::S_VW;
+  // shared memory here: the lane-predicated task loops read the constant
+  // copy slower (measured c4 0.82 vs 0.92 G edges/s)
+  const double* vphi = vol_tables<C, false>(st);
+  const double* vdphi = vphi + (C::S_VDPHI - C::S_VPHI);
+  const double* vw = vphi + (C::S_VW - C::S_VPHI);
 #pragma unroll 1
   for (int q0 = 0; q0 < C::NQV; q0 += QCH) {
     const int nq = (C::NQV - q0) < QCH ? (C::NQV - q0) : QCH;
@@ -644,7 +674,6 @@ __device__ __forceinline__ void surface_tasks(const double* st, double* ws, cons
     for (int g = 0; g < C::NQF; ++g) {
       double tr = 0.0;
       if (c.has) {
-#pragma unroll
         tr = dot_row<C::NP>(fphi + g * C::NPP, u);
       } else if (c.valid && ln.side == 1) {
         tr = prm.ff[ln.eq];  // far-field ghost state on physical boundaries

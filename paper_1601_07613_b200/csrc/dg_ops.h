@@ -22,6 +22,9 @@ struct Ops {
   cudaError_t (*init)(Ops* self);   // occupancy queries, smem opt-in
   int stable_size;                  // doubles of the padded table layout
   cudaError_t (*stage_global)(const double* tables, double* out, cudaStream_t s);
+  // copy the volume part of the padded tables into this configuration's
+  // constant-memory array (c_voltab)
+  cudaError_t (*upload_const)(const double* ptables_dev);
 };
 
 // defined in dg_tri.cu / dg_quad.cu / dg_tet.cu; nullptr if not compiled
@@ -131,11 +134,17 @@ struct Instance {
     k_stage_global<C><<<1, 256, smem, s>>>(tables, out);
     return cudaGetLastError();
   }
+  static cudaError_t upload_const(const double* ptables_dev) {
+    // the volume tables depend on (kind, degree) only: both physics share one
+    return cudaMemcpyToSymbol(c_voltab<K, P>, ptables_dev + C::S_VPHI,
+                              sizeof(double) * (C::S_SIZE - C::S_VPHI), 0,
+                              cudaMemcpyDeviceToDevice);
+  }
   static Ops* ops() {
     static Ops o{C::DIM, C::NEQ, C::NP, C::NQF, C::NQV, C::NCODES, C::T_SIZE,
                  T::OK ? T::THREADS : C::THREADS, T::OK ? T::SW : C::SPW,
                  0, 0, 0, &colored, &volume, &uncolored, &gather, &init, C::S_TOTAL,
-                 &stage_global};
+                 &stage_global, &upload_const};
     return &o;
   }
 };

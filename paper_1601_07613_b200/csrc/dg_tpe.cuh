@@ -122,9 +122,9 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
                                            bool mine, const Params& P,
                                            double (&acc)[Tpe<C>::WH]) {
   constexpr int WH = Tpe<C>::WH, NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH, DIM = C::DIM;
-  const double* vphi = st + C::S_VPHI;
-  const double* vdphi = st + C::S_VDPHI;
-  const double* vw = st + C::S_VW;
+  const double* vphi = vol_tables<C, Tpe<C>::H == 1>(st);
+  const double* vdphi = vphi + (C::S_VDPHI - C::S_VPHI);
+  const double* vw = vphi + (C::S_VW - C::S_VPHI);
   double ji[DIM * DIM];
 #pragma unroll
   for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
