@@ -115,6 +115,11 @@ __device__ __forceinline__ double own_part(const double* v, int h, int k) {
   }
 }
 
+#ifndef MC_VOL_UNROLL
+#define MC_VOL_UNROLL 1
+#endif
+constexpr int kVolUnroll = MC_VOL_UNROLL;   // volume-point loop unroll (A/B knob)
+
 // Volume integral of this lane's element (its equations), added into acc.
 template <class C, int PH>
 __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[Tpe<C>::WH],
@@ -128,7 +133,7 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   double ji[DIM * DIM];
 #pragma unroll
   for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
-#pragma unroll 1
+#pragma unroll kVolUnroll
   for (int q = 0; q < C::NQV; ++q) {
     double own[NEQH], s[NEQ];
 #pragma unroll
@@ -393,6 +398,9 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 #ifndef MC_TPE_MINB_RK
 #define MC_TPE_MINB_RK 3
 #endif
+#ifndef MC_TPE_MINB_VOL
+#define MC_TPE_MINB_VOL 0   // 0: Tpe<C>::MINB
+#endif
 
 struct TpeLane {
   int lane, side, h, grp, nown, eq0;
@@ -416,7 +424,8 @@ __device__ __forceinline__ TpeLane tpe_lane() {
 // variant per color launch so surface-only passes carry no volume code.
 template <class C, int PH, bool kRK, bool kVol>
 __global__ void __launch_bounds__(Tpe<C>::THREADS,
-                                  (kVol || Tpe<C>::H == 2) ? Tpe<C>::MINB
+                                  Tpe<C>::H == 2 ? Tpe<C>::MINB
+                                  : kVol ? (MC_TPE_MINB_VOL ? MC_TPE_MINB_VOL : Tpe<C>::MINB)
                                   : (kRK ? MC_TPE_MINB_RK : MC_TPE_MINB_SURF))
 k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
               int64_t end) {
