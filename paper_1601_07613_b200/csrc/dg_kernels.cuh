@@ -152,10 +152,11 @@ struct Cfg {
 // from S_VPHI on.  Every lane of a warp reads the same entry at the same
 // time (uniform index), so these become uniform-datapath loads (LDCU) that
 // cost no shared-memory wavefronts.  One array per configuration; filled by
-// Instance::upload_const at operator creation.  Used by the one-lane-per-
-// element-side register kernel (c2: 3.43 -> 3.53 G edges/s); the group and
-// two-lane kernels keep the shared-memory copy (slower from constant memory:
-// c4 0.92 -> 0.82, c3 0.94 -> 0.92).  MC_SMEM_VOLTAB forces shared memory.
+// Instance::upload_const at operator creation.  Used by the register
+// kernels (c2: 3.43 -> 3.53 G edges/s, c3: 0.94 -> 0.97 with warp-uniform
+// control flow around the reads); the group kernel keeps the shared-memory
+// copy (from constant memory c4 drops 0.92 -> 0.81, even with uniform
+// loops).  MC_SMEM_VOLTAB forces shared memory.
 template <int K, int P>
 __constant__ double c_voltab[Cfg<K, ADV, P>::S_SIZE - Cfg<K, ADV, P>::S_VPHI];
 
