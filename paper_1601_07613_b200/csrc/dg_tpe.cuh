@@ -48,6 +48,11 @@ struct Tpe {
   static constexpr bool OK = H == 1 || (H == 2 && PAIRS && C::DIM == 2);
 #endif
 #endif
+  // 256-bit accesses for every lane's run: 32-byte aligned offsets and
+  // lengths (blocks are 32-byte padded); H = 2 when both equation groups
+  // span a multiple of four coefficients (c3: 2 x 16)
+  static constexpr bool V4 = (H == 1 && W % 4 == 0) ||
+                             (H == 2 && (NEQH * C::NP) % 4 == 0 && (NEQ1 * C::NP) % 4 == 0);
   static constexpr int SW = 16 / (H ? H : 1);                      // surfaces per warp
   static constexpr int THREADS = 128;
 #ifdef MC_MINB_TPE
@@ -324,12 +329,16 @@ __device__ __forceinline__ void st4(double* p, double a, double b, double c, dou
 
 // This lane's run of `n` doubles (n <= N): the whole block when H = 1
 // (256-bit when N % 4 == 0), its equation group when H = 2 (128-bit pairs).
-template <int N, bool kWhole>
+template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0)>
 __device__ __forceinline__ void tload(const double* __restrict__ src, int n, double (&dst)[N]) {
-  if constexpr (kWhole && N % 4 == 0) {
+  if constexpr (kV4) {
 #pragma unroll
-    for (int j = 0; j < N / 4; ++j)
-      ld4_nc(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
+    for (int j = 0; j < N / 4; ++j) {
+      if (kWhole || 4 * j < n)
+        ld4_nc(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
+      else
+        dst[4 * j] = dst[4 * j + 1] = dst[4 * j + 2] = dst[4 * j + 3] = 0.0;
+    }
   } else if constexpr (N % 2 == 0) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
@@ -348,12 +357,16 @@ __device__ __forceinline__ void tload(const double* __restrict__ src, int n, dou
   }
 }
 
-template <int N, bool kWhole>
+template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0)>
 __device__ __forceinline__ void tload_rw(const double* src, int n, double (&dst)[N]) {
-  if constexpr (kWhole && N % 4 == 0) {
+  if constexpr (kV4) {
 #pragma unroll
-    for (int j = 0; j < N / 4; ++j)
-      ld4(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
+    for (int j = 0; j < N / 4; ++j) {
+      if (kWhole || 4 * j < n)
+        ld4(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
+      else
+        dst[4 * j] = dst[4 * j + 1] = dst[4 * j + 2] = dst[4 * j + 3] = 0.0;
+    }
   } else if constexpr (N % 2 == 0) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
@@ -372,12 +385,13 @@ __device__ __forceinline__ void tload_rw(const double* src, int n, double (&dst)
   }
 }
 
-template <int N, bool kWhole>
+template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0)>
 __device__ __forceinline__ void tstore(double* dst, int n, const double (&src)[N]) {
-  if constexpr (kWhole && N % 4 == 0) {
+  if constexpr (kV4) {
 #pragma unroll
     for (int j = 0; j < N / 4; ++j)
-      st4(dst + 4 * j, src[4 * j], src[4 * j + 1], src[4 * j + 2], src[4 * j + 3]);
+      if (kWhole || 4 * j < n)
+        st4(dst + 4 * j, src[4 * j], src[4 * j + 1], src[4 * j + 2], src[4 * j + 3]);
   } else if constexpr (N % 2 == 0) {
     double2* d2 = reinterpret_cast<double2*>(dst);
 #pragma unroll
@@ -450,12 +464,12 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
     const bool last = kRK && t.owner && (t.code & (ln.side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
     const int64_t off = int64_t(t.has ? t.e : 0) * v.stride + ln.eq0 * C::NP;
     double u[WH], acc[WH];
-    if (t.has) tload<WH, kWhole>(U + off, n, u);
+    if (t.has) tload<WH, kWhole, T::V4>(U + off, n, u);
     else {
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
     }
-    if (t.owner && !first) tload_rw<WH, kWhole>(R + off, n, acc);
+    if (t.owner && !first) tload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     else {
 #pragma unroll
       for (int j = 0; j < WH; ++j) acc[j] = 0.0;
@@ -471,19 +485,19 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
     tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc);
     if (t.owner) {
       if (last) {
-        if (rk.save_u0) tstore<WH, kWhole>(rk.U0 + off, n, u);
+        if (rk.save_u0) tstore<WH, kWhole, T::V4>(rk.U0 + off, n, u);
         if (rk.a != 0.0) {
           double u0[WH];
-          tload<WH, kWhole>(rk.U0 + off, n, u0);
+          tload<WH, kWhole, T::V4>(rk.U0 + off, n, u0);
 #pragma unroll
           for (int j = 0; j < WH; ++j) acc[j] = rk.a * u0[j] + rk.b * fma(rk.dt, acc[j], u[j]);
         } else {
 #pragma unroll
           for (int j = 0; j < WH; ++j) acc[j] = rk.b * fma(rk.dt, acc[j], u[j]);
         }
-        tstore<WH, kWhole>(U + off, n, acc);
+        tstore<WH, kWhole, T::V4>(U + off, n, acc);
       } else {
-        tstore<WH, kWhole>(R + off, n, acc);
+        tstore<WH, kWhole, T::V4>(R + off, n, acc);
       }
     }
   }
@@ -506,7 +520,7 @@ k_tpe_uncolored(View v, const double* __restrict__ U, double* __restrict__ out) 
     const int64_t s = tile + ln.grp;
     const TpeSide t = tpe_side<C>(v, s, end, ln.side);
     double u[WH], acc[WH];
-    if (t.has) tload<WH, kWhole>(U + int64_t(t.e) * v.stride + ln.eq0 * C::NP, n, u);
+    if (t.has) tload<WH, kWhole, T::V4>(U + int64_t(t.e) * v.stride + ln.eq0 * C::NP, n, u);
     else {
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
@@ -526,7 +540,7 @@ k_tpe_uncolored(View v, const double* __restrict__ U, double* __restrict__ out) 
 #pragma unroll
         for (int j = 0; j < WH; ++j) acc[j] = 0.0;
       }
-      tstore<WH, kWhole>(out + (2 * s + ln.side) * v.stride + ln.eq0 * C::NP, n, acc);
+      tstore<WH, kWhole, T::V4>(out + (2 * s + ln.side) * v.stride + ln.eq0 * C::NP, n, acc);
     }
   }
 }
@@ -550,7 +564,7 @@ k_tpe_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
     const bool has = e < v.n_elements;
     const int64_t off = (has ? e : 0) * v.stride + eq0 * C::NP;
     double u[WH], acc[WH];
-    if (has) tload<WH, kWhole>(U + off, n, u);
+    if (has) tload<WH, kWhole, T::V4>(U + off, n, u);
     else {
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
@@ -559,7 +573,7 @@ k_tpe_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
     for (int j = 0; j < WH; ++j) acc[j] = 0.0;
     tpe_volume<C, PH>(st, u, v.jinv + (has ? e : 0) * (C::DIM * C::DIM), h, nown, has, v.prm,
                       acc);
-    if (has) tstore<WH, kWhole>(R + off, n, acc);
+    if (has) tstore<WH, kWhole, T::V4>(R + off, n, acc);
   }
 }
 
