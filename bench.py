@@ -190,7 +190,9 @@ def kernel_name(op) -> str:
     w = op.n_equations * op.n_basis
     if w <= 24:
         return "k_tpe_colored (1 lane per element side)"
-    if w <= 64 and op.dim == 2 and op.n_equations >= 2:
+    neqh = (op.n_equations + 1) // 2
+    pairs = op.n_basis % 2 == 0 or (neqh % 2 == 0 and (op.n_equations - neqh) % 2 == 0)
+    if w <= 64 and op.n_equations >= 2 and pairs:
         return "k_tpe_colored (2 lanes per element side)"
     return "k_surface_colored (2*N_eq lanes per surface, warp flux tasks)"
 

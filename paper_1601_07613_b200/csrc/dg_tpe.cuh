@@ -40,12 +40,12 @@ struct Tpe {
 #ifdef MC_TPE_H1_ONLY
   static constexpr bool OK = H == 1;
 #else
-  // tets keep the group kernel: with 27 volume points the 2x redundant flux
-  // of H = 2 loses to the task scheme (measured)
-#ifdef MC_TPE_TET
-  static constexpr bool OK = H == 1 || (H == 2 && PAIRS);
-#else
+#ifdef MC_TET_GROUP
   static constexpr bool OK = H == 1 || (H == 2 && PAIRS && C::DIM == 2);
+#else
+  // tets too since the volume tables moved to constant memory (c4: 1.01 vs
+  // 0.93 G edges/s for the group kernel); MC_TET_GROUP restores the latter
+  static constexpr bool OK = H == 1 || (H == 2 && PAIRS);
 #endif
 #endif
   // 256-bit accesses for every lane's run: 32-byte aligned offsets and
