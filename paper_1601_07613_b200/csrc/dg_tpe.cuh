@@ -33,7 +33,11 @@ struct Tpe {
   static constexpr int W = C::NEQ * C::NP;
   static constexpr int H = (W <= 24) ? 1 : ((W <= 64 && C::NEQ >= 2) ? 2 : 0);
   static constexpr int NEQH = H ? (C::NEQ + H - 1) / H : C::NEQ;   // eqs of lane h = 0
-  static constexpr int NEQ1 = C::NEQ - NEQH;                       // eqs of lane h = 1
+  static constexpr int NEQ1 = C::NEQ - NEQH;
+  // H = 2: lane h = 0 holds equations [0, NA), lane h = 1 holds [NA, NEQ)
+  // (NA <= NEQH: with an odd count the second lane takes the larger group,
+  // so both runs start 32-byte aligned for tets, 2 + 3 equations x 10)
+  static constexpr int NA = (H == 2) ? NEQ1 : NEQH;
   static constexpr int WH = NEQH * C::NP;                          // doubles per lane
   // H = 2 moves 16-byte pairs: every lane's run must have even length
   static constexpr bool PAIRS = (C::NP % 2 == 0) || (NEQH % 2 == 0 && NEQ1 % 2 == 0);
@@ -52,7 +56,7 @@ struct Tpe {
   // lengths (blocks are 32-byte padded); H = 2 when both equation groups
   // span a multiple of four coefficients (c3: 2 x 16)
   static constexpr bool V4 = (H == 1 && W % 4 == 0) ||
-                             (H == 2 && (NEQH * C::NP) % 4 == 0 && (NEQ1 * C::NP) % 4 == 0);
+                             (H == 2 && (NA * C::NP) % 4 == 0 && (NEQH * C::NP) % 2 == 0);
   static constexpr int SW = 16 / (H ? H : 1);                      // surfaces per warp
   static constexpr int THREADS = 128;
 #ifdef MC_MINB_TPE
@@ -102,9 +106,11 @@ __device__ __forceinline__ void assemble_state(const double (&own)[Tpe<C>::NEQH]
 #pragma unroll
     for (int k = 0; k < NEQH; ++k) oth[k] = __shfl_xor_sync(kFull, own[k], 1);
 #pragma unroll
+    constexpr int NA = Tpe<C>::NA;
+#pragma unroll
     for (int e = 0; e < C::NEQ; ++e)
-      s[e] = (e < NEQH) ? (h == 0 ? own[e] : oth[e])
-                        : (h == 1 ? own[e - NEQH] : oth[e - NEQH]);
+      s[e] = (e < NA) ? (h == 0 ? own[e] : oth[e])
+                      : (h == 1 ? own[e - NA] : oth[e - NA]);
   }
 }
 
@@ -115,7 +121,8 @@ __device__ __forceinline__ double own_part(const double* v, int h, int k) {
   if constexpr (Tpe<C>::H == 1) {
     return v[k];
   } else {
-    const int e1 = (NEQH + k < C::NEQ) ? NEQH + k : C::NEQ - 1;
+    constexpr int NA = Tpe<C>::NA;
+    const int e1 = (NA + k < C::NEQ) ? NA + k : C::NEQ - 1;
     return h == 0 ? v[k] : v[e1];
   }
 }
@@ -237,7 +244,7 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
   const double* fphi = st + C::S_FPHI + t.mycode * (C::NQF * C::NPP);
   const double* fw = st + C::S_FW;
   const double sc = -t.scale;
-  const int eq0 = h * NEQH;
+  const int eq0 = h * Tpe<C>::NA;
   double nO[C::DIM];
 #pragma unroll
   for (int d = 0; d < C::DIM; ++d) nO[d] = side ? -t.n[d] : t.n[d];
@@ -331,13 +338,22 @@ __device__ __forceinline__ void st4(double* p, double a, double b, double c, dou
 // (256-bit when N % 4 == 0), its equation group when H = 2 (128-bit pairs).
 template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0)>
 __device__ __forceinline__ void tload(const double* __restrict__ src, int n, double (&dst)[N]) {
-  if constexpr (kV4) {
+  if constexpr (kV4) {   // 32-byte chunks, a 16-byte tail when N % 4 == 2
 #pragma unroll
     for (int j = 0; j < N / 4; ++j) {
-      if (kWhole || 4 * j < n)
+      if (kWhole || 4 * j + 4 <= n)
         ld4_nc(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
       else
         dst[4 * j] = dst[4 * j + 1] = dst[4 * j + 2] = dst[4 * j + 3] = 0.0;
+    }
+    if constexpr (N % 4 == 2) {
+      if (kWhole || N <= n) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(src + N - 2));
+        dst[N - 2] = a.x;
+        dst[N - 1] = a.y;
+      } else {
+        dst[N - 2] = dst[N - 1] = 0.0;
+      }
     }
   } else if constexpr (N % 2 == 0) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
@@ -362,10 +378,19 @@ __device__ __forceinline__ void tload_rw(const double* src, int n, double (&dst)
   if constexpr (kV4) {
 #pragma unroll
     for (int j = 0; j < N / 4; ++j) {
-      if (kWhole || 4 * j < n)
+      if (kWhole || 4 * j + 4 <= n)
         ld4(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
       else
         dst[4 * j] = dst[4 * j + 1] = dst[4 * j + 2] = dst[4 * j + 3] = 0.0;
+    }
+    if constexpr (N % 4 == 2) {
+      if (kWhole || N <= n) {
+        const double2 a = *reinterpret_cast<const double2*>(src + N - 2);
+        dst[N - 2] = a.x;
+        dst[N - 1] = a.y;
+      } else {
+        dst[N - 2] = dst[N - 1] = 0.0;
+      }
     }
   } else if constexpr (N % 2 == 0) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
@@ -390,8 +415,11 @@ __device__ __forceinline__ void tstore(double* dst, int n, const double (&src)[N
   if constexpr (kV4) {
 #pragma unroll
     for (int j = 0; j < N / 4; ++j)
-      if (kWhole || 4 * j < n)
+      if (kWhole || 4 * j + 4 <= n)
         st4(dst + 4 * j, src[4 * j], src[4 * j + 1], src[4 * j + 2], src[4 * j + 3]);
+    if constexpr (N % 4 == 2)
+      if (kWhole || N <= n)
+        *reinterpret_cast<double2*>(dst + N - 2) = make_double2(src[N - 2], src[N - 1]);
   } else if constexpr (N % 2 == 0) {
     double2* d2 = reinterpret_cast<double2*>(dst);
 #pragma unroll
@@ -432,8 +460,8 @@ __device__ __forceinline__ TpeLane tpe_lane() {
   L.grp = L.lane / (2 * H);
   L.side = (L.lane / H) & 1;
   L.h = L.lane % H;
-  L.eq0 = L.h * Tpe<C>::NEQH;
-  L.nown = (L.h == 0) ? Tpe<C>::NEQH : Tpe<C>::NEQ1;
+  L.eq0 = L.h * Tpe<C>::NA;
+  L.nown = (L.h == 0) ? Tpe<C>::NA : Tpe<C>::NEQH;
   return L;
 }
 
@@ -556,7 +584,7 @@ k_tpe_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
   extern __shared__ double st[];
   tpe_stage<C>(v.tables, st);
   const int lane = threadIdx.x & 31, h = lane % H;
-  const int nown = (h == 0) ? T::NEQH : T::NEQ1, eq0 = h * T::NEQH, n = nown * C::NP;
+  const int nown = (h == 0) ? T::NA : T::NEQH, eq0 = h * T::NA, n = nown * C::NP;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t tile = warp * (32 / H); tile < v.n_elements; tile += nwarp * (32 / H)) {

@@ -5,5 +5,5 @@ run() {  # $1 = defines, $2 = env assignment
 }
 rm -f gpurun_out/ab_summary.txt
 python -m pytest tests -m gpu -x -q 2>&1 | tail -1 >> gpurun_out/ab_summary.txt
-for cfg in c4; do export BENCH_ARGS="--config $cfg"; for d in ""; do run "$d" "X=1"; done; done
+for cfg in c4 c3; do export BENCH_ARGS="--config $cfg"; for d in ""; do run "$d" "X=1"; done; done
 cat gpurun_out/ab_summary.txt
