@@ -114,7 +114,7 @@ for i, d in enumerate(launches):
     al = algo[i % len(algo)] / 1e6
     traffic.append((rd + wr) * 1e6)
     lines.append(f"| color {i % len(algo) + 1} | {d['Kernel Name'].split('<')[0]} | "
-                 f"{float(d['gpu__time_duration.sum'].replace(',', '')) * {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}.get(ui['gpu__time_duration.sum'], 1.0):.1f} | "
+                 f"{float(d['gpu__time_duration.sum'].replace(',', '')) * {'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1.0, 'us': 1.0, 'msecond': 1e3, 'ms': 1e3}.get(ui['gpu__time_duration.sum'], 1.0):.1f} | "
                  f"{rd:.0f} | {wr:.0f} | {al:.0f} | {(rd + wr) / al:.2f} | "
                  f"{d.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', '')} | "
                  f"{d['sm__warps_active.avg.pct_of_peak_sustained_active']} | "
