@@ -286,6 +286,7 @@ struct Physics;
 template <int DIM, int NEQ>
 struct Physics<ADV, DIM, NEQ> {
   // Fhat . n (upwind = Lax-Friedrichs with lambda = |a.n|)
+  template <bool kFast = true>
   __device__ static __forceinline__ void lf(const double* sL, const double* sR, const double* n,
                                             const Params& P, double* out) {
     double an = P.vel[0] * n[0] + P.vel[1] * n[1];
@@ -293,6 +294,7 @@ struct Physics<ADV, DIM, NEQ> {
     out[0] = 0.5 * an * (sL[0] + sR[0]) - 0.5 * fabs(an) * (sR[0] - sL[0]);
   }
   // contravariant flux Ft[r][k] = sum_d Jinv[r][d] F_d(s)[k]
+  template <bool kFast = true>
   __device__ static __forceinline__ void vflux(const double* s, const double* ji,
                                                const Params& P, double* Ft) {
 #pragma unroll
@@ -350,9 +352,10 @@ __device__ __forceinline__ double flux_sqrt(double x) {
 
 template <int DIM, int NEQ>
 struct Physics<EULER, DIM, NEQ> {
-  // measured: the Newton forms win in the 2D register kernels (c2 +1 %,
-  // c3 +2 %) and lose in the 3D group kernel (c4 -5 %, register pressure)
-  static constexpr bool kFast = DIM == 2;
+  // kFast: Newton-refined MUFU reciprocal / square root.  Measured: wins in
+  // the register kernels (c2 +1 %, c3 +2 %, c4 +3 %), loses in the group
+  // kernel (-5 %, register pressure), which passes false.
+  template <bool kFast = true>
   __device__ static __forceinline__ void prim(const double* s, const Params& P, double* u,
                                               double& p, double& inv) {
     inv = flux_rcp<kFast>(s[0]);
@@ -365,11 +368,12 @@ struct Physics<EULER, DIM, NEQ> {
     p = (P.gamma - 1.0) * (s[NEQ - 1] - 0.5 * ke);
   }
 
+  template <bool kFast = true>
   __device__ static __forceinline__ void lf(const double* sL, const double* sR, const double* n,
                                             const Params& P, double* out) {
     double uL[DIM], uR[DIM], pL, pR, iL, iR;
-    prim(sL, P, uL, pL, iL);
-    prim(sR, P, uR, pR, iR);
+    prim<kFast>(sL, P, uL, pL, iL);
+    prim<kFast>(sR, P, uR, pR, iR);
     double vnL = 0.0, vnR = 0.0;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
@@ -391,10 +395,11 @@ struct Physics<EULER, DIM, NEQ> {
                    0.5 * lam * (sR[NEQ - 1] - sL[NEQ - 1]);
   }
 
+  template <bool kFast = true>
   __device__ static __forceinline__ void vflux(const double* s, const double* ji,
                                                const Params& P, double* Ft) {
     double u[DIM], p, inv;
-    prim(s, P, u, p, inv);
+    prim<kFast>(s, P, u, p, inv);
 #pragma unroll
     for (int r = 0; r < DIM; ++r) {
       double ut = 0.0;
@@ -477,7 +482,7 @@ __device__ __forceinline__ void volume_tasks(const double* st, double* vs, doubl
         double s[C::NEQ], Ft[C::DIM * C::NEQ];
 #pragma unroll
         for (int k = 0; k < C::NEQ; ++k) s[k] = vs[t * C::SV + k];
-        Physics<PH, C::DIM, C::NEQ>::vflux(s, ji + e * C::JIS, prm, Ft);
+        Physics<PH, C::DIM, C::NEQ>::template vflux<false>(s, ji + e * C::JIS, prm, Ft);
         const double w = vw[q0 + qq];
 #pragma unroll
         for (int r = 0; r < C::DIM; ++r) {
@@ -559,7 +564,7 @@ __device__ __forceinline__ void volume_dmma(const double* st, double* ws, const 
           const int row = 4 * h + qq, g = swz8(row);
 #pragma unroll
           for (int k = 0; k < C::NEQ; ++k) sv[k] = vq[row * 32 + ((e * C::NEQ + k) ^ g)];
-          Physics<PH, C::DIM, C::NEQ>::vflux(sv, ji + e * C::JIS, prm, Ft);
+          Physics<PH, C::DIM, C::NEQ>::template vflux<false>(sv, ji + e * C::JIS, prm, Ft);
           const double w = vw[q];
 #pragma unroll
           for (int k = 0; k < C::DIM * C::NEQ; ++k) Ft[k] *= w;
@@ -704,7 +709,7 @@ __device__ __forceinline__ void surface_tasks(const double* st, double* ws, cons
       }
 #pragma unroll
       for (int d = 0; d < C::DIM; ++d) n[d] = flip ? -n[d] : n[d];
-      Physics<PH, C::DIM, C::NEQ>::lf(cL, cR, n, prm, out);
+      Physics<PH, C::DIM, C::NEQ>::template lf<false>(cL, cR, n, prm, out);
       const double w = flip ? -fw[g] : fw[g];
 #pragma unroll
       for (int k = 0; k < C::NEQ; ++k) ws[C::W_FS + t * C::SV + k] = w * out[k];

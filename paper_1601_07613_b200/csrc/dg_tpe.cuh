@@ -154,7 +154,7 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
     const double w = vw[q];
     if constexpr (Tpe<C>::H == 1 && PH == EULER) {
       // whole block in this lane: fluxes straight into the projection
-      const double inv = flux_rcp<C::DIM == 2>(s[0]);
+      const double inv = flux_rcp<true>(s[0]);
       double vel[DIM], ke = 0.0;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
