@@ -127,10 +127,13 @@ __device__ __forceinline__ double own_part(const double* v, int h, int k) {
   }
 }
 
-#ifndef MC_VOL_UNROLL
-#define MC_VOL_UNROLL 1
+// volume-point loop unroll: 2 for two lanes per side (c3 1.12 -> 1.15 G
+// edges/s, c4 neutral), 1 for one lane (registers); MC_VOL_UNROLL overrides
+#ifdef MC_VOL_UNROLL
+template <int H> constexpr int kVolUnroll = MC_VOL_UNROLL;
+#else
+template <int H> constexpr int kVolUnroll = H == 2 ? 2 : 1;
 #endif
-constexpr int kVolUnroll = MC_VOL_UNROLL;   // volume-point loop unroll (A/B knob)
 
 // Volume integral of this lane's element (its equations), added into acc.
 template <class C, int PH>
@@ -145,7 +148,8 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   double ji[DIM * DIM];
 #pragma unroll
   for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
-#pragma unroll kVolUnroll
+  constexpr int kUnroll = kVolUnroll<Tpe<C>::H>;
+#pragma unroll kUnroll
   for (int q = 0; q < C::NQV; ++q) {
     double own[NEQH], s[NEQ];
 #pragma unroll
