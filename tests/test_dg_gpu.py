@@ -61,7 +61,7 @@ def test_rhs_all_strategies_match_oracle(cuda, kind, physics, p, build, period):
         assert rel_terms(got, want, prob, U) < TOL, (strategy, rel(got, want))
 
 
-@pytest.mark.parametrize("ordering", ["reorder", "renumber", "none"])
+@pytest.mark.parametrize("ordering", ["sfc", "reorder", "renumber", "none"])
 @pytest.mark.parametrize("palette", ["minimal", "naive"])
 def test_layouts_and_palettes(cuda, ordering, palette):
     build = lambda: P.shuffle_elements(P.gen_tri_rect(12, 9), 2)
