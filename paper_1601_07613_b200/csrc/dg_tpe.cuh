@@ -230,6 +230,34 @@ __device__ __forceinline__ TpeSide tpe_side(const View& v, int64_t s, int64_t en
   return t;
 }
 
+// As tpe_side, with this lane's element id already loaded (one tile ahead:
+// the element-block loads of a tile then wait on one DRAM round trip, not
+// on the index load and then the block load).
+template <class C>
+__device__ __forceinline__ TpeSide tpe_side_pre(const View& v, int64_t s, int64_t end, int side,
+                                                int e_pre) {
+  TpeSide t;
+  t.valid = s < end;
+  t.code = 0;
+  t.scale = 0.0;
+  t.n[0] = 1.0;
+  t.n[1] = 0.0;
+  t.n[2] = 0.0;
+  if (t.valid) {
+    t.code = __ldg(v.code + s);
+    const double* gm = v.geom + s * C::GEOM;
+#pragma unroll
+    for (int d = 0; d < C::DIM; ++d) t.n[d] = __ldg(gm + d);
+    t.scale = __ldg(gm + C::DIM + side);
+  }
+  t.e = t.valid ? e_pre : -1;
+  t.boundary = side && t.e < 0;
+  t.has = t.valid && t.e >= 0;
+  t.owner = t.has && !(side && (t.code & MC_FLAG_R_GHOST));
+  t.mycode = side ? int((t.code >> 6) & 63u) : int(t.code & 63u);
+  return t;
+}
+
 // Surface contribution of this lane (side, equation group), added into acc.
 // All lanes call (shuffles).  Each side evaluates the flux OUT of its own
 // element, F_own = lf(own state, other state, own outward normal): no
@@ -489,9 +517,25 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
   const int n = ln.nown * C::NP;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
+#ifndef MC_NO_E_PREFETCH
+  const int32_t* eidx = ln.side ? v.right : v.left;
+  int e_next = -1;
+  {
+    const int64_t s0 = begin + warp * T::SW + ln.grp;
+    if (s0 < end) e_next = __ldg(eidx + s0);
+  }
+#endif
   for (int64_t tile = begin + warp * T::SW; tile < end; tile += nwarp * T::SW) {
     const int64_t s = tile + ln.grp;
+#ifndef MC_NO_E_PREFETCH
+    const TpeSide t = tpe_side_pre<C>(v, s, end, ln.side, e_next);
+    {
+      const int64_t sn = s + nwarp * T::SW;
+      e_next = sn < end ? __ldg(eidx + sn) : -1;
+    }
+#else
     const TpeSide t = tpe_side<C>(v, s, end, ln.side);
+#endif
     const bool first = kVol && t.owner && (t.code & (ln.side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
     const bool last = kRK && t.owner && (t.code & (ln.side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
     const int64_t off = int64_t(t.has ? t.e : 0) * v.stride + ln.eq0 * C::NP;
