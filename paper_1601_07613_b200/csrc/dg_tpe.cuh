@@ -148,6 +148,70 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   double ji[DIM * DIM];
 #pragma unroll
   for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
+#ifndef MC_NO_QUAD_SF
+  if constexpr (C::KIND == QUAD && Tpe<C>::H == 2) {
+    // tensor-product quads: sum factorisation (basis l_i(x) l_j(y), Gauss
+    // points (x_a, y_b)), half the multiply-adds of the dense contraction.
+    //   trace:      T[j] = sum_i l_i(x_a) u[i][j];  U(a,b) = sum_j l_j(y_b) T[j]
+    //   projection: A[j] += w_ab l_j(y_b) F0, B[j] += w_ab l'_j(y_b) F1 over b,
+    //               then acc[i][j] += l'_i(x_a) A[j] + l_i(x_a) B[j]
+    // The 1D values are entries of the 2D tables (l_0 = 1 for the
+    // orthonormal basis on [0,1]).
+    constexpr int n = C::PDEG + 1;
+    static_assert(n * n == NP && n * n == C::NQV, "tensor quad layout");
+    auto L1 = [&](int a, int i) { return vphi[(a * n) * C::NPP + i * n]; };
+    auto D1 = [&](int a, int i) { return vdphi[(a * n) * C::NPP + i * n]; };
+#pragma unroll 1
+    for (int a = 0; a < n; ++a) {
+      double T[NEQH][n], A[NEQH][n], B[NEQH][n];
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k)
+#pragma unroll
+        for (int j = 0; j < n; ++j) {
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < n; ++i) t = fma(L1(a, i), u[k * NP + i * n + j], t);
+          T[k][j] = t;
+          A[k][j] = 0.0;
+          B[k][j] = 0.0;
+        }
+#pragma unroll
+      for (int b = 0; b < n; ++b) {
+        double own[NEQH], s[NEQ], Ft[DIM * NEQ];
+#pragma unroll
+        for (int k = 0; k < NEQH; ++k) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < n; ++j) t = fma(L1(b, j), T[k][j], t);
+          own[k] = t;
+        }
+        assemble_state<C>(own, h, s);
+        Physics<PH, DIM, NEQ>::vflux(s, ji, P, Ft);
+        const double w = vw[a * n + b];
+#pragma unroll
+        for (int k = 0; k < NEQH; ++k) {
+          const bool on = mine && k < nown;
+          const double g0 = on ? w * own_part<C>(Ft, h, k) : 0.0;
+          const double g1 = on ? w * own_part<C>(Ft + NEQ, h, k) : 0.0;
+#pragma unroll
+          for (int j = 0; j < n; ++j) {
+            A[k][j] = fma(L1(b, j), g0, A[k][j]);
+            B[k][j] = fma(D1(b, j), g1, B[k][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k)
+#pragma unroll
+        for (int i = 0; i < n; ++i)
+#pragma unroll
+          for (int j = 0; j < n; ++j)
+            acc[k * NP + i * n + j] =
+                fma(D1(a, i), A[k][j], fma(L1(a, i), B[k][j], acc[k * NP + i * n + j]));
+    }
+    return;
+  }
+#endif
   constexpr int kUnroll = kVolUnroll<Tpe<C>::H>;
 #pragma unroll kUnroll
   for (int q = 0; q < C::NQV; ++q) {
