@@ -37,6 +37,10 @@ CASES = [
     ("quad", "euler", 1, lambda: P.gen_quad_rect(4, 4, (True, True)), (4, 4)),
     ("quad", "euler", 2, lambda: P.shuffle_elements(P.gen_quad_rect(5, 6), 3), None),
     ("quad", "euler", 3, lambda: P.gen_quad_rect(6, 5), None),
+    ("quad", "euler", 2, lambda: P.gen_quad_rect(6, 6, (True, True)), (6, 6)),
+    ("tri", "euler", 4, lambda: P.shuffle_elements(P.gen_tri_rect(5, 4), 2), None),
+    ("tet", "euler", 3, lambda: P.gen_tet_prism(2, 2, 1), None),
+    ("tet", "advection", 2, lambda: P.shuffle_elements(P.gen_tet_prism(2, 2, 2), 1), None),
     ("tet", "advection", 1, lambda: P.gen_tet_prism(2, 2, 2), None),
     ("tet", "advection", 3, lambda: P.gen_tet_prism(2, 1, 2), None),
     ("tet", "euler", 1, lambda: P.gen_tet_prism(2, 2, 1), None),
