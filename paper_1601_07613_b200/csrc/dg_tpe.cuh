@@ -322,6 +322,39 @@ __device__ __forceinline__ TpeSide tpe_side_pre(const View& v, int64_t s, int64_
   return t;
 }
 
+// Lax-Friedrichs flux out of this lane's element with the per-state work
+// shared across the surface: each side forms the primitive quantities of
+// its OWN state (velocity, pressure, normal velocity, sound speed) and
+// takes the other side's (p, c, -v.n) from the partner lane (xor H).  The
+// values are bit-identical to evaluating both states here (the partner's
+// normal velocity is computed with the negated normal: an exact negation),
+// so each lane's result still depends only on its element's view.
+template <int PH, int DIM, int NEQ, int H>
+__device__ __forceinline__ void lf_shared(const double* s, const double* x, const double* n,
+                                          const Params& P, double* out) {
+  if constexpr (PH != EULER) {
+    Physics<PH, DIM, NEQ>::lf(s, x, n, P, out);
+  } else {
+    double uo[DIM], po, io;
+    Physics<PH, DIM, NEQ>::template prim<true>(s, P, uo, po, io);
+    double vo = 0.0;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) vo += uo[d] * n[d];
+    const double co = flux_sqrt<true>(P.gamma * po * io);
+    const double vx = -__shfl_xor_sync(kFull, vo, H);
+    const double px = __shfl_xor_sync(kFull, po, H);
+    const double cx = __shfl_xor_sync(kFull, co, H);
+    const double lam = fmax(fabs(vo) + co, fabs(vx) + cx);
+    out[0] = 0.5 * (s[0] * vo + x[0] * vx) - 0.5 * lam * (x[0] - s[0]);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+      out[1 + d] = 0.5 * ((s[1 + d] * vo + po * n[d]) + (x[1 + d] * vx + px * n[d])) -
+                   0.5 * lam * (x[1 + d] - s[1 + d]);
+    out[NEQ - 1] = 0.5 * ((s[NEQ - 1] + po) * vo + (x[NEQ - 1] + px) * vx) -
+                   0.5 * lam * (x[NEQ - 1] - s[NEQ - 1]);
+  }
+}
+
 // Surface contribution of this lane (side, equation group), added into acc.
 // All lanes call (shuffles).  Each side evaluates the flux OUT of its own
 // element, F_own = lf(own state, other state, own outward normal): no
@@ -363,7 +396,11 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
       double x[NEQ], out[NEQ];
 #pragma unroll
       for (int k = 0; k < NEQ; ++k) x[k] = __shfl_xor_sync(kFull, trc[g][k], 1);
+#ifdef MC_NO_LF_SHARE
       Physics<PH, C::DIM, NEQ>::lf(trc[g], x, nO, P, out);
+#else
+      lf_shared<PH, C::DIM, NEQ, 1>(trc[g], x, nO, P, out);
+#endif
       if (t.owner) {
         const double c = sc * fw[g];
 #pragma unroll
@@ -399,7 +436,11 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
       assemble_state<C>(own, h, s);
 #pragma unroll
       for (int k = 0; k < NEQ; ++k) x[k] = __shfl_xor_sync(kFull, s[k], H);
+#ifdef MC_NO_LF_SHARE
       Physics<PH, C::DIM, NEQ>::lf(s, x, nO, P, out);
+#else
+      lf_shared<PH, C::DIM, NEQ, H>(s, x, nO, P, out);
+#endif
       if (t.owner) {
         const double c = sc * fw[g];
 #pragma unroll

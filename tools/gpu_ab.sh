@@ -5,5 +5,5 @@ run() {  # $1 = defines, $2 = env assignment
 }
 rm -f gpurun_out/ab_summary.txt
 python -m pytest tests/test_dg_gpu.py tests/test_partition_gpu.py tests/test_convergence_gpu.py -x -q 2>&1 | tail -1 >> gpurun_out/ab_summary.txt
-for cfg in c3; do export BENCH_ARGS="--config $cfg"; for d in "" "MC_NO_QUAD_SF"; do run "$d" "X=1"; done; done
+for cfg in c2 c4 c3; do export BENCH_ARGS="--config $cfg"; for d in ""; do run "$d" "X=1"; done; done
 cat gpurun_out/ab_summary.txt
