@@ -43,34 +43,46 @@ UNIT = "edges/s"
 
 
 # ------------------------------------------------------------- workloads
+def _setup_device():
+    """Mesh assembly / AMR setup on the GPU when one is visible (untimed
+    setup; bit-identical to the host path), else on the host."""
+    try:
+        from paper_1601_07613_b200 import _native
+        return "cuda" if _native.lib().mc_device_count() > 0 else None
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def config_spec(name: str):
     import paper_1601_07613_b200 as P
+    dv = _setup_device()
     if name == "c1":
         return dict(desc="2D scalar advection DG p=1, gen_tri_rect(64,64), 3 colors",
                     build=lambda: P.gen_tri_rect(64, 64), physics="advection", p=1,
                     sample=lambda: P.gen_tri_rect(64, 64))
     if name == "c2":
         return dict(desc="2D Euler DG p=2, shuffle_elements(gen_tri_rect(708,708),0), LF, 3 colors",
-                    build=lambda: P.shuffle_elements(P.gen_tri_rect(708, 708), 0),
+                    build=lambda: P.shuffle_elements(P.gen_tri_rect(708, 708, device=dv), 0, device=dv),
                     physics="euler", p=2,
                     sample=lambda: P.shuffle_elements(P.gen_tri_rect(177, 177), 0),
                     # weak scaling: N stacked c2 slabs, one per GPU
-                    weak=lambda n: P.shuffle_elements(P.gen_tri_rect(708, 708 * n), 0))
+                    weak=lambda n: P.shuffle_elements(P.gen_tri_rect(708, 708 * n, device=dv), 0,
+                                                      device=dv))
     if name == "c3":
         return dict(desc="2D Euler DG p=3, gen_quad_rect(2000,2000), LF, 4 colors",
-                    build=lambda: P.gen_quad_rect(2000, 2000), physics="euler", p=3,
+                    build=lambda: P.gen_quad_rect(2000, 2000, device=dv), physics="euler", p=3,
                     sample=lambda: P.gen_quad_rect(250, 250))
     if name == "c4":
         return dict(desc="3D Euler DG p=2, gen_tet_prism(110,110,110), LF, 4 colors",
-                    build=lambda: P.gen_tet_prism(110, 110, 110), physics="euler", p=2,
+                    build=lambda: P.gen_tet_prism(110, 110, 110, device=dv), physics="euler", p=2,
                     sample=lambda: P.gen_tet_prism(28, 28, 28))
     if name == "c5":
         def build():
-            base = P.gen_tri_rect(708, 708)
+            base = P.gen_tri_rect(708, 708, device=dv)
             col, _ = P.color(base)
             cen = base.vertices[base.elem_verts[:, :3]].mean(axis=1)
             tg = np.flatnonzero(((cen - 354.0) ** 2).sum(1) <= 177.0 ** 2)
-            return P.refine(base, col, tg)
+            return P.refine(base, col, tg, device=dv)
 
         def sample():
             base = P.gen_tri_rect(177, 177)
