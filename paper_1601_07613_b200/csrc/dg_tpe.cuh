@@ -64,7 +64,26 @@ struct Tpe {
 #else
   static constexpr int MINB = (H == 2) ? 2 : ((W > 16) ? 3 : 4);
 #endif
-  static constexpr int SMEM = C::S_TOTAL * 8;
+  // two lanes per side on tets: fluxes as warp tasks (c4 1.17 -> 1.22 G
+  // edges/s); quads keep the per-lane flux (c3 neutral, its first-touch
+  // color slower).  MC_NO_H2_TASKS / MC_H2_TASKS_ALL for A/B.
+#if defined(MC_NO_H2_TASKS)
+  static constexpr bool TASKS = false;
+#elif defined(MC_H2_TASKS_ALL)
+  static constexpr bool TASKS = (H == 2);
+#else
+  static constexpr bool TASKS = (H == 2 && C::DIM == 3);
+#endif
+  // per-warp scratch of the task-packed surface flux (TASKS): traces
+  // [NQF][SW][2][SV], canonical fluxes [NQF][SW][SV], normals [SW][DIM],
+  // flags [SW] (ints); SV odd
+  static constexpr int SV = C::NEQ | 1;
+  static constexpr int X_TR = 0;
+  static constexpr int X_FS = X_TR + C::NQF * (16 / (H ? H : 1)) * 2 * SV;
+  static constexpr int X_NRM = X_FS + C::NQF * (16 / (H ? H : 1)) * SV;
+  static constexpr int X_FLG = X_NRM + (16 / (H ? H : 1)) * C::DIM;
+  static constexpr int X_SIZE = (X_FLG + (16 / (H ? H : 1)) / 2 + 2) & ~1;
+  static constexpr int SMEM = (C::S_TOTAL + (TASKS ? 4 * X_SIZE : 0)) * 8;
 };
 
 template <int NP, int N>
@@ -367,7 +386,8 @@ __device__ __forceinline__ void lf_shared(const double* s, const double* x, cons
 template <class C, int PH>
 __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, int side, int h,
                                             int nown, const double (&u)[Tpe<C>::WH],
-                                            const Params& P, double (&acc)[Tpe<C>::WH]) {
+                                            const Params& P, double (&acc)[Tpe<C>::WH],
+                                            int grp = 0, double* ws = nullptr) {
   constexpr int NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH;
   constexpr int H = Tpe<C>::H;
   const double* fphi = st + C::S_FPHI + t.mycode * (C::NQF * C::NPP);
@@ -382,7 +402,75 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
   // the surface-only colors of c2.  H = 2: per point, the basis row is read
   // once into registers and used for both the trace and the lift (c3: 0.94
   // vs 0.88 G edges/s for the trace-first form).
-  if constexpr (H == 1) {
+  if constexpr (Tpe<C>::TASKS) {
+    // Two lanes per side, fluxes packed as warp tasks: every lane writes its
+    // traces to the warp scratch, the warp's (surface, point) fluxes are
+    // evaluated once each (SW * NQF tasks over 32 lanes) in the canonical
+    // (single-domain) orientation, and each lane lifts its equations with
+    // the sign of its canonical side: bit-identical under partitioning.
+    constexpr int SW = Tpe<C>::SW, SV = Tpe<C>::SV;
+    double* tr = ws + Tpe<C>::X_TR;
+    double* fs = ws + Tpe<C>::X_FS;
+    double* nrm = ws + Tpe<C>::X_NRM;
+    int* flg = reinterpret_cast<int*>(ws + Tpe<C>::X_FLG);
+    const int lane = threadIdx.x & 31;
+    const bool flip = (t.code & MC_FLAG_FLIPPED) != 0;
+    if (side == 0 && h == 0) {
+      flg[grp] = t.valid ? (flip ? 2 : 1) : 0;
+#pragma unroll
+      for (int d = 0; d < C::DIM; ++d) nrm[grp * C::DIM + d] = t.n[d];
+    }
+#pragma unroll 1
+    for (int g = 0; g < C::NQF; ++g) {
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k) {
+        if (k < nown) {
+          const double v = t.has ? tdot<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP)
+                                 : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
+          tr[((g * SW + grp) * 2 + side) * SV + eq0 + k] = v;
+        }
+      }
+    }
+    __syncwarp();
+    for (int q = lane; q < SW * C::NQF; q += 32) {
+      const int g = q / SW, gs = q - g * SW;
+      const int f = flg[gs];
+      if (f) {
+        double sL[NEQ], sR[NEQ], cL[NEQ], cR[NEQ], nn[C::DIM], out[NEQ];
+#pragma unroll
+        for (int e = 0; e < NEQ; ++e) {
+          sL[e] = tr[((g * SW + gs) * 2 + 0) * SV + e];
+          sR[e] = tr[((g * SW + gs) * 2 + 1) * SV + e];
+        }
+        const bool fl = f == 2;
+#pragma unroll
+        for (int e = 0; e < NEQ; ++e) {
+          cL[e] = fl ? sR[e] : sL[e];
+          cR[e] = fl ? sL[e] : sR[e];
+        }
+#pragma unroll
+        for (int d = 0; d < C::DIM; ++d) nn[d] = fl ? -nrm[gs * C::DIM + d] : nrm[gs * C::DIM + d];
+        Physics<PH, C::DIM, NEQ>::lf(cL, cR, nn, P, out);
+#pragma unroll
+        for (int e = 0; e < NEQ; ++e) fs[(g * SW + gs) * SV + e] = out[e];
+      }
+    }
+    __syncwarp();
+    if (t.owner) {
+      // canonical left loses F, canonical right gains it
+      const double sc2 = ((side != 0) != flip) ? t.scale : -t.scale;
+#pragma unroll 1
+      for (int g = 0; g < C::NQF; ++g) {
+        const double c = sc2 * fw[g];
+#pragma unroll
+        for (int k = 0; k < NEQH; ++k)
+          if (k < nown)
+            taxpy<NP, Tpe<C>::WH>(fphi + g * C::NPP, c * fs[(g * SW + grp) * SV + eq0 + k], acc,
+                                  k * NP);
+      }
+    }
+    __syncwarp();
+  } else if constexpr (H == 1) {
     double trc[C::NQF][NEQH];
 #pragma unroll
     for (int g = 0; g < C::NQF; ++g) {
@@ -604,6 +692,9 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 #ifndef MC_TPE_MINB_RK
 #define MC_TPE_MINB_RK 3
 #endif
+#ifndef MC_TASKS_MINB_SURF
+#define MC_TASKS_MINB_SURF 2
+#endif
 #ifndef MC_TPE_MINB_VOL
 #define MC_TPE_MINB_VOL 0   // 0: Tpe<C>::MINB
 #endif
@@ -630,7 +721,9 @@ __device__ __forceinline__ TpeLane tpe_lane() {
 // variant per color launch so surface-only passes carry no volume code.
 template <class C, int PH, bool kRK, bool kVol>
 __global__ void __launch_bounds__(Tpe<C>::THREADS,
-                                  Tpe<C>::H == 2 ? Tpe<C>::MINB
+                                  Tpe<C>::H == 2
+                                      ? ((Tpe<C>::TASKS && !kVol && !kRK) ? MC_TASKS_MINB_SURF
+                                                                           : Tpe<C>::MINB)
                                   : kVol ? (MC_TPE_MINB_VOL ? MC_TPE_MINB_VOL : Tpe<C>::MINB)
                                   : (kRK ? MC_TPE_MINB_RK : MC_TPE_MINB_SURF))
 k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
@@ -641,6 +734,7 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
   extern __shared__ double sts[];
   tpe_stage<C>(v.tables, sts);
   const double* st = sts;
+  double* ws = sts + C::S_TOTAL + (threadIdx.x >> 5) * T::X_SIZE;   // TASKS scratch
   const TpeLane ln = tpe_lane<C>();
   const int n = ln.nown * C::NP;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -686,7 +780,7 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
         tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc);
       }
     }
-    tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc);
+    tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc, ln.grp, ws);
     if (t.owner) {
       if (last) {
         if (rk.save_u0) tstore<WH, kWhole, T::V4>(rk.U0 + off, n, u);
@@ -715,6 +809,7 @@ k_tpe_uncolored(View v, const double* __restrict__ U, double* __restrict__ out) 
   constexpr bool kWhole = T::H == 1;
   extern __shared__ double st[];
   tpe_stage<C>(v.tables, st);
+  double* ws = st + C::S_TOTAL + (threadIdx.x >> 5) * T::X_SIZE;   // TASKS scratch
   const TpeLane ln = tpe_lane<C>();
   const int n = ln.nown * C::NP;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -731,7 +826,7 @@ k_tpe_uncolored(View v, const double* __restrict__ U, double* __restrict__ out) 
     }
 #pragma unroll
     for (int j = 0; j < WH; ++j) acc[j] = 0.0;
-    tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc);
+    tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc, ln.grp, ws);
     if (kAtomic) {
       if (t.owner) {
         double* dst = out + int64_t(t.e) * v.stride + ln.eq0 * C::NP;
