@@ -32,6 +32,7 @@ from .meshio import (NativeMesh, read_msh, read_native, write_native,
                      write_report)
 from .reorder import (CoalescingReport, ReorderingPlan, apply_plan, build_plan,
                       coalescing_metric, invert_plan)
+from .scaling import ScalingPoint, ScalingSeries, fit_loglog_slope, run_series
 from .sweeps import (AccumulationState, MemoryEstimate, assert_race_free,
                      basis_count, default_payload, memory_saved,
                      surface_buffer, sweep_atomic, sweep_buffered,
