@@ -45,11 +45,11 @@ struct Instance {
       if (krk && has_first)
         k_tpe_colored<C, PH, true, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
       else if (krk)
-        k_tpe_colored<C, PH, true, false><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
+        k_tpe_colored<C, PH, true, false><<<grid, T::THREADS, T::SMEM_SURF, s>>>(v, U, R, r, b, e);
       else if (has_first)
         k_tpe_colored<C, PH, false, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
       else
-        k_tpe_colored<C, PH, false, false><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
+        k_tpe_colored<C, PH, false, false><<<grid, T::THREADS, T::SMEM_SURF, s>>>(v, U, R, r, b, e);
     } else {
       if (rk)
         k_surface_colored<C, PH, true><<<grid, C::THREADS, C::SMEM, s>>>(v, U, R, *rk, b, e);
@@ -105,10 +105,11 @@ struct Instance {
     int g2 = 0;
     if constexpr (T::OK) {
       if ((err = fit((const void*)k_tpe_colored<C, PH, true, true>, T::SMEM, T::THREADS, &o->grid_colored))) return err;
+      if ((err = fit((const void*)k_tpe_colored<C, PH, false, true>, T::SMEM, T::THREADS, &g2))) return err;
+      if (g2 < o->grid_colored) o->grid_colored = g2;
       for (const void* fn : {(const void*)k_tpe_colored<C, PH, true, false>,
-                             (const void*)k_tpe_colored<C, PH, false, true>,
                              (const void*)k_tpe_colored<C, PH, false, false>}) {
-        if ((err = fit(fn, T::SMEM, T::THREADS, &g2))) return err;
+        if ((err = fit(fn, T::SMEM_SURF, T::THREADS, &g2))) return err;
         if (g2 < o->grid_colored) o->grid_colored = g2;
       }
       if ((err = fit((const void*)k_tpe_volume<C, PH>, T::SMEM, T::THREADS, &o->grid_volume))) return err;

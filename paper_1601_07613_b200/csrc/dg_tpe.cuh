@@ -83,7 +83,17 @@ struct Tpe {
   static constexpr int X_NRM = X_FS + C::NQF * (16 / (H ? H : 1)) * SV;
   static constexpr int X_FLG = X_NRM + (16 / (H ? H : 1)) * C::DIM;
   static constexpr int X_SIZE = (X_FLG + (16 / (H ? H : 1)) / 2 + 2) & ~1;
+  // two-lane 2D kernels: task-packed fluxes in the surface-only and
+  // last-touch passes only (c3 surface colors +2.5 %); their first-touch
+  // pass keeps the per-lane flux and the small shared-memory footprint.
+  // MC_NO_SURF_TASKS for A/B.
+#ifdef MC_NO_SURF_TASKS
+  static constexpr bool TASKS_SURF = TASKS;
+#else
+  static constexpr bool TASKS_SURF = TASKS || H == 2;
+#endif
   static constexpr int SMEM = (C::S_TOTAL + (TASKS ? 4 * X_SIZE : 0)) * 8;
+  static constexpr int SMEM_SURF = (C::S_TOTAL + (TASKS_SURF ? 4 * X_SIZE : 0)) * 8;
 };
 
 template <int NP, int N>
@@ -383,7 +393,7 @@ __device__ __forceinline__ void lf_shared(const double* s, const double* x, cons
 // contributions without special handling.  The two sides' values are
 // negatives of each other up to rounding (the oracle's single flux times
 // -/+1 agrees to ~1e-16 relative).
-template <class C, int PH>
+template <class C, int PH, bool kTasks = Tpe<C>::TASKS>
 __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, int side, int h,
                                             int nown, const double (&u)[Tpe<C>::WH],
                                             const Params& P, double (&acc)[Tpe<C>::WH],
@@ -402,7 +412,7 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
   // the surface-only colors of c2.  H = 2: per point, the basis row is read
   // once into registers and used for both the trace and the lift (c3: 0.94
   // vs 0.88 G edges/s for the trace-first form).
-  if constexpr (Tpe<C>::TASKS) {
+  if constexpr (kTasks) {
     // Two lanes per side, fluxes packed as warp tasks: every lane writes its
     // traces to the warp scratch, the warp's (surface, point) fluxes are
     // evaluated once each (SW * NQF tasks over 32 lanes) in the canonical
@@ -780,7 +790,8 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
         tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc);
       }
     }
-    tpe_surface<C, PH>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc, ln.grp, ws);
+    tpe_surface<C, PH, (kVol ? T::TASKS : T::TASKS_SURF)>(st, t, ln.side, ln.h, ln.nown, u, v.prm,
+                                                          acc, ln.grp, ws);
     if (t.owner) {
       if (last) {
         if (rk.save_u0) tstore<WH, kWhole, T::V4>(rk.U0 + off, n, u);
