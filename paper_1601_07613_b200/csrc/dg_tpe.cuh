@@ -732,7 +732,7 @@ __device__ __forceinline__ TpeLane tpe_lane() {
 template <class C, int PH, bool kRK, bool kVol>
 __global__ void __launch_bounds__(Tpe<C>::THREADS,
                                   Tpe<C>::H == 2
-                                      ? ((Tpe<C>::TASKS && !kVol && !kRK) ? MC_TASKS_MINB_SURF
+                                      ? ((!kVol && !kRK) ? MC_TASKS_MINB_SURF
                                                                            : Tpe<C>::MINB)
                                   : kVol ? (MC_TPE_MINB_VOL ? MC_TPE_MINB_VOL : Tpe<C>::MINB)
                                   : (kRK ? MC_TPE_MINB_RK : MC_TPE_MINB_SURF))
