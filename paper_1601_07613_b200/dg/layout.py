@@ -188,7 +188,8 @@ def _normals(kind, Xl, local_l, surf_pts_l, centroid):
 
 def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
                        period=None, mortars=None, owned=None, flipped=None,
-                       code_sort=False) -> SurfaceList:
+                       code_sort=False, code_sort_window: int = 0,
+                       code_sort_skip_first: bool = False) -> SurfaceList:
     """Assemble the device surface list from a color-grouped mesh.
 
     ``colors`` must be non-decreasing over surface ids (a mesh produced by
@@ -199,6 +200,9 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
     side codes (stable), so the lanes of a warp read the same reference-face
     table rows (shared-memory broadcasts).  Any order within a color is
     race free and leaves every element's accumulation order unchanged.
+    ``code_sort_window`` > 0 sorts by code only inside consecutive windows of
+    that many surfaces (keeps the element-ascending order at a coarse scale);
+    ``code_sort_skip_first`` leaves color 1 (the coalesced color) unsorted.
     """
     kind = mesh_kind(mesh)
     dim = DIM[kind]
@@ -321,6 +325,10 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
         # partitioned: surfaces touching a ghost go last in their color, so
         # the rest of the first color can run while the ghosts are exchanged
         key2 = (code & 0xFFF) if code_sort else np.zeros(len(sid), dtype=np.int64)
+        if code_sort and code_sort_window > 0:
+            key2 = key2 + (np.arange(len(sid), dtype=np.int64) // code_sort_window) * 4096
+        if code_sort and code_sort_skip_first:
+            key2 = np.where(col == 1, 0, key2)
         perm = np.lexsort((np.arange(len(sid)), key2, ghost_r.astype(np.int64), col))
         L, R, code, geom, col, sid = L[perm], R[perm], code[perm], geom[perm], col[perm], sid[perm]
         has_r, ghost_r, loc_l, loc_r = has_r[perm], ghost_r[perm], loc_l[perm], loc_r[perm]
