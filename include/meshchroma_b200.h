@@ -198,6 +198,11 @@ int mc_dg_destroy(mc_dg* dg);
 /* doubles between consecutive element blocks (block padded to 32 B) */
 int64_t mc_dg_block_stride(const mc_dg* dg);
 int64_t mc_dg_buffer_bytes(const mc_dg* dg); /* buffered-variant scratch */
+/* Upper bound on the blocks of every persistent-grid launch (0 = the
+ * occupancy-sized default).  A small cap makes every warp loop over many
+ * surface tiles even on a small mesh (the loop-carried path production
+ * runs), which is what the parity tests use it for. */
+int mc_dg_set_grid_cap(mc_dg* dg, int max_blocks);
 
 /* R := RHS(U) on owned elements.  Colored: volume fused into each
  * element's first color pass, surfaces one launch per color, no atomics,
@@ -227,8 +232,25 @@ int mc_dg_color_range_pass(mc_dg* dg, int color, int64_t begin, int64_t end,
 /* n_steps SSP-RK3 steps; work_dev = 2 blocks arrays (U0, R scratch). */
 int mc_dg_ssprk3(mc_dg* dg, double* U_dev, double* work_dev, double dt,
                  int n_steps, void* stream);
-/* End-to-end: copy U from host, n_steps SSP-RK3 steps, copy back. */
+/* End-to-end: copy U from host, n_steps SSP-RK3 steps, copy back (U_host
+ * in the internal layout). */
 int mc_dg_ssprk3_host(mc_dg* dg, double* U_host, double dt, int n_steps);
+
+/* Caller (user) element order — what the reference-facing API takes:
+ * arrays of n_user_rows x (N_eq * N_p) doubles, one unpadded row per element
+ * in the caller's numbering.  src[r] (n_elements entries) is the user row
+ * of internal owned row r (the inverse of reorder.build_plan's
+ * element_perm for a single domain; the owned global ids on a partition). */
+int mc_dg_set_user_rows(mc_dg* dg, const int64_t* src_host, int64_t n_user_rows);
+/* Device permutations between the two layouts (internal padding zeroed). */
+int mc_dg_user_to_internal(mc_dg* dg, const double* user_dev, double* U_dev, void* stream);
+int mc_dg_internal_to_user(mc_dg* dg, const double* U_dev, double* user_dev, void* stream);
+/* End-to-end in the user layout (DGOperator.ssprk3 / .rhs): H2D of the
+ * caller's array, device permutation, the colored steps (or one RHS with the
+ * given strategy), permutation back, D2H.  Single-domain operators only. */
+int mc_dg_ssprk3_user_host(mc_dg* dg, double* U_user_host, double dt, int n_steps);
+int mc_dg_rhs_user_host(mc_dg* dg, const double* U_user_host, double* R_user_host,
+                        int strategy);
 
 /* ------------------------------------------------------------------ */
 /* Surface extraction (mesh.assemble, reference mesh.py:207-300)       */

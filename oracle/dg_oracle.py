@@ -340,13 +340,16 @@ def setup(prob: Problem):
     return c
 
 
-def volume_term(prob: Problem, U: np.ndarray) -> np.ndarray:
-    """U (ne, neq, nb) -> volume contribution (ne, neq, nb)."""
+def volume_term(prob: Problem, U: np.ndarray, lo: int = 0, hi: int | None = None
+                ) -> np.ndarray:
+    """U (ne, neq, nb) -> volume contribution (ne, neq, nb); with lo/hi
+    the elements [lo, hi) only (U still indexed globally)."""
     c = setup(prob)
-    Uq = np.einsum("qj,ekj->eqk", c["vphi"], U)
+    hi = len(U) if hi is None else hi
+    Uq = np.einsum("qj,ekj->eqk", c["vphi"], U[lo:hi])
     F = prob.physics.flux(Uq)                                  # (e, q, d, k)
-    Ft = np.einsum("erd,eqdk->eqrk", c["Jinv"], F)             # contravariant
-    return np.einsum("q,rqj,eqrk->ekj", c["vW"], c["vdphi"], Ft)
+    Ft = np.einsum("erd,eqdk->eqrk", c["Jinv"][lo:hi], F)      # contravariant
+    return np.einsum("q,rqj,eqrk->ekj", c["vW"], c["vdphi"], Ft, optimize=True)
 
 
 def surface_contributions(prob: Problem, U: np.ndarray, sel=None):

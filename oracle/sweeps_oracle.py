@@ -3,6 +3,9 @@
 Follows /root/reference/pkg/src/meshchroma/sweeps.py:
   default_payload   :55-62   splitmix64 mix of k = 1..n, top 20 bits, centred
   sweep_sequential  :74-86   totals[L] += f, totals[R] -= f, id order
+  sweep_colored     :114-152 per color, surfaces in id order split into
+                             `workers` contiguous chunks run by a thread
+                             pool, joined before the next color
   assert_race_free  :89-105  first color with a repeated element
   surface_buffer    :155-176 slots 2k / 2k+1
   sweep_buffered    :179-204 per-element gather in local side order
@@ -60,6 +63,39 @@ def sweep_sequential_loop(surf_elems, n_elements, payload) -> np.ndarray:
         tot[l] += v
         if r >= 0:
             tot[r] -= v
+    return np.asarray(tot, dtype=np.int64)
+
+
+def sweep_colored_threads(surf_elems, n_elements, payload, colors, n_colors,
+                          workers: int) -> np.ndarray:
+    """The reference's threaded colored sweep restated: interpreted
+    per-surface updates on shared Python lists, one thread-pool round per
+    color (the inter-color barrier), ``workers`` contiguous chunks per
+    color.  Race free by the coloring; the GIL serialises the work, which
+    is what the reference's CPU path measures."""
+    from concurrent.futures import ThreadPoolExecutor
+    tot = [0] * n_elements
+    left = surf_elems[:, 0].tolist()
+    right = surf_elems[:, 1].tolist()
+    vals = payload.tolist()
+    colors = np.asarray(colors)
+
+    def work(ids):
+        for s in ids:
+            tot[left[s]] += vals[s]
+            r = right[s]
+            if r >= 0:
+                tot[r] -= vals[s]
+
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        for c in range(1, n_colors + 1):
+            ids = np.flatnonzero(colors == c).tolist()
+            if not ids:
+                continue
+            step = max(1, -(-len(ids) // workers))
+            futs = [pool.submit(work, ids[a:a + step]) for a in range(0, len(ids), step)]
+            for f in futs:
+                f.result()
     return np.asarray(tot, dtype=np.int64)
 
 

@@ -35,6 +35,14 @@ struct mc_dg {
   double *g_U = nullptr, *g_work = nullptr;
   double g_dt = 0.0;
   cudaStream_t g_stream = nullptr;
+  // upper bound on the blocks of every persistent-grid launch (0 = none):
+  // lets tests make each warp loop over many tiles on a small mesh
+  int grid_cap = 0;
+  // caller (user) element order: internal owned row r <- user row src[r]
+  int64_t* d_user_src = nullptr;
+  int64_t n_user_rows = 0;
+  double* d_user = nullptr;        // user-layout staging (n_user_rows x W)
+  double* d_user_R = nullptr;      // user-layout residual staging
 };
 
 namespace {
@@ -65,7 +73,43 @@ int colored_grid(const mc_dg* h, int64_t n) {
   int grid = h->ops->grid_colored;
   static const bool full = std::getenv("MC_FULL_GRID") != nullptr;   // A/B knob
   if (full || grid > max_blocks) grid = int(std::min<int64_t>(max_blocks, 1 << 30));
+  if (h->grid_cap > 0 && grid > h->grid_cap) grid = h->grid_cap;
   return grid < 1 ? 1 : grid;
+}
+
+int capped(const mc_dg* h, int grid) {
+  return (h->grid_cap > 0 && grid > h->grid_cap) ? h->grid_cap : grid;
+}
+
+// user layout (n_user_rows x W, W = N_eq*N_p doubles per element, caller
+// order) <-> internal layout (renumbered rows, `stride`-padded blocks); one
+// thread per internal double, coalesced on the internal side, W contiguous
+// doubles per row on the user side
+__global__ void k_user_to_internal(const double* __restrict__ user, const int64_t* __restrict__ src,
+                                   double* __restrict__ U, int64_t rows, int W, int stride) {
+  const int64_t total = rows * stride;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / stride;
+    const int j = int(i - r * stride);
+    U[i] = j < W ? __ldg(user + __ldg(src + r) * W + j) : 0.0;
+  }
+}
+
+__global__ void k_internal_to_user(const double* __restrict__ U, const int64_t* __restrict__ src,
+                                   double* __restrict__ user, int64_t rows, int W, int stride) {
+  const int64_t total = rows * W;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / W;
+    const int j = int(i - r * W);
+    user[__ldg(src + r) * W + j] = U[r * stride + j];
+  }
+}
+
+int copy_grid(int64_t total) {
+  const int64_t g = (total + 255) / 256;
+  return int(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
 }
 
 int colored_pass(mc_dg* h, double* U, double* R, const mcdg::RK* rk, cudaStream_t s) {
@@ -208,6 +252,9 @@ MC_API int mc_dg_destroy(mc_dg* h) {
   cudaFree(h->d_slots);
   cudaFree(h->d_buffer);
   cudaFree(h->d_host_U);
+  cudaFree(h->d_user_src);
+  cudaFree(h->d_user);
+  cudaFree(h->d_user_R);
   if (h->step_exec) cudaGraphExecDestroy(h->step_exec);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -215,6 +262,16 @@ MC_API int mc_dg_destroy(mc_dg* h) {
 }
 
 MC_API int64_t mc_dg_block_stride(const mc_dg* h) { return h ? h->stride : -1; }
+
+MC_API int mc_dg_set_grid_cap(mc_dg* h, int max_blocks) {
+  if (!h || max_blocks < 0) return mc_fail(MC_EINVAL, "bad argument");
+  h->grid_cap = max_blocks;
+  if (h->step_exec) {   // the captured step baked the old grid sizes in
+    cudaGraphExecDestroy(h->step_exec);
+    h->step_exec = nullptr;
+  }
+  return MC_OK;
+}
 
 MC_API int64_t mc_dg_buffer_bytes(const mc_dg* h) {
   return h ? 2 * h->ns * h->stride * int64_t(sizeof(double)) : -1;
@@ -227,16 +284,16 @@ MC_API int mc_dg_rhs(mc_dg* h, const double* U, double* R, int strategy, void* s
   if (strategy == MC_DG_COLORED) return colored_pass(h, Um, R, nullptr, s);
   if (strategy != MC_DG_BUFFERED && strategy != MC_DG_ATOMIC)
     return mc_fail(MC_EINVAL, "unknown strategy");
-  int gv = h->ops->grid_volume;
+  const int gv = capped(h, h->ops->grid_volume), gu = capped(h, h->ops->grid_uncolored);
   DG_TRY(h->ops->volume(h->view, U, R, gv, s));
   if (strategy == MC_DG_ATOMIC) {
-    if (h->ns) DG_TRY(h->ops->uncolored(h->view, U, R, true, h->ops->grid_uncolored, s));
+    if (h->ns) DG_TRY(h->ops->uncolored(h->view, U, R, true, gu, s));
     return MC_OK;
   }
   if (!h->d_slot_ptr) return mc_fail(MC_EINVAL, "buffered strategy needs the element slot CSR");
   if (!h->d_buffer) DG_TRY(cudaMalloc(&h->d_buffer, size_t(mc_dg_buffer_bytes(h)) + 16));
-  if (h->ns) DG_TRY(h->ops->uncolored(h->view, U, h->d_buffer, false, h->ops->grid_uncolored, s));
-  DG_TRY(h->ops->gather(h->view, h->d_buffer, R, s));
+  if (h->ns) DG_TRY(h->ops->uncolored(h->view, U, h->d_buffer, false, gu, s));
+  DG_TRY(h->ops->gather(h->view, h->d_buffer, R, h->grid_cap, s));
   return MC_OK;
 }
 
@@ -348,6 +405,86 @@ MC_API int mc_dg_ssprk3_host(mc_dg* h, double* U_host, double dt, int n_steps) {
   if (int rc = mc_dg_ssprk3(h, h->d_host_U, h->d_host_U + nblk, dt, n_steps, h->stream)) return rc;
   DG_TRY(cudaMemcpyAsync(U_host, h->d_host_U, sizeof(double) * h->ne * h->stride,
                          cudaMemcpyDeviceToHost, h->stream));
+  DG_TRY(cudaStreamSynchronize(h->stream));
+  return MC_OK;
+}
+
+MC_API int mc_dg_set_user_rows(mc_dg* h, const int64_t* src, int64_t n_user_rows) {
+  if (!h || !src || n_user_rows < 1) return mc_fail(MC_EINVAL, "bad argument");
+  for (int64_t r = 0; r < h->ne; ++r)
+    if (src[r] < 0 || src[r] >= n_user_rows)
+      return mc_fail(MC_EINVAL, "user row " + std::to_string(src[r]) + " out of range");
+  cudaFree(h->d_user_src);
+  cudaFree(h->d_user);
+  cudaFree(h->d_user_R);
+  h->d_user = h->d_user_R = nullptr;
+  h->d_user_src = nullptr;
+  h->n_user_rows = 0;
+  DG_TRY(upload(&h->d_user_src, src, h->ne));
+  h->n_user_rows = n_user_rows;
+  return MC_OK;
+}
+
+MC_API int mc_dg_user_to_internal(mc_dg* h, const double* user_dev, double* U_dev, void* stream) {
+  if (!h || !user_dev || !U_dev) return mc_fail(MC_EINVAL, "null argument");
+  if (!h->d_user_src) return mc_fail(MC_EINVAL, "user row map not set (mc_dg_set_user_rows)");
+  const int W = h->ops->neq * h->ops->np;
+  k_user_to_internal<<<copy_grid(h->ne * h->stride), 256, 0, as_stream(stream)>>>(
+      user_dev, h->d_user_src, U_dev, h->ne, W, int(h->stride));
+  DG_TRY(cudaGetLastError());
+  return MC_OK;
+}
+
+MC_API int mc_dg_internal_to_user(mc_dg* h, const double* U_dev, double* user_dev, void* stream) {
+  if (!h || !user_dev || !U_dev) return mc_fail(MC_EINVAL, "null argument");
+  if (!h->d_user_src) return mc_fail(MC_EINVAL, "user row map not set (mc_dg_set_user_rows)");
+  const int W = h->ops->neq * h->ops->np;
+  k_internal_to_user<<<copy_grid(h->ne * W), 256, 0, as_stream(stream)>>>(
+      U_dev, h->d_user_src, user_dev, h->ne, W, int(h->stride));
+  DG_TRY(cudaGetLastError());
+  return MC_OK;
+}
+
+namespace {
+int user_staging(mc_dg* h, bool residual) {
+  if (!h->d_user_src) return mc_fail(MC_EINVAL, "user row map not set (mc_dg_set_user_rows)");
+  const int64_t nblk = (h->ne + h->ng) * h->stride;
+  const size_t ubytes = sizeof(double) * size_t(h->n_user_rows) * h->ops->neq * h->ops->np;
+  if (!h->d_host_U) DG_TRY(cudaMalloc(&h->d_host_U, sizeof(double) * size_t(3 * nblk)));
+  if (!h->d_user) DG_TRY(cudaMalloc(&h->d_user, ubytes));
+  if (residual && !h->d_user_R) DG_TRY(cudaMalloc(&h->d_user_R, ubytes));
+  if (!h->stream) DG_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  return MC_OK;
+}
+}  // namespace
+
+MC_API int mc_dg_ssprk3_user_host(mc_dg* h, double* U_host, double dt, int n_steps) {
+  if (!h || !U_host) return mc_fail(MC_EINVAL, "null argument");
+  if (h->ng) return mc_fail(MC_EINVAL, "partitioned operator: use the device entry points");
+  if (int rc = user_staging(h, false)) return rc;
+  const int64_t nblk = (h->ne + h->ng) * h->stride;
+  const size_t ubytes = sizeof(double) * size_t(h->n_user_rows) * h->ops->neq * h->ops->np;
+  DG_TRY(cudaMemcpyAsync(h->d_user, U_host, ubytes, cudaMemcpyHostToDevice, h->stream));
+  if (int rc = mc_dg_user_to_internal(h, h->d_user, h->d_host_U, h->stream)) return rc;
+  if (int rc = mc_dg_ssprk3(h, h->d_host_U, h->d_host_U + nblk, dt, n_steps, h->stream)) return rc;
+  if (int rc = mc_dg_internal_to_user(h, h->d_host_U, h->d_user, h->stream)) return rc;
+  DG_TRY(cudaMemcpyAsync(U_host, h->d_user, ubytes, cudaMemcpyDeviceToHost, h->stream));
+  DG_TRY(cudaStreamSynchronize(h->stream));
+  return MC_OK;
+}
+
+MC_API int mc_dg_rhs_user_host(mc_dg* h, const double* U_host, double* R_host, int strategy) {
+  if (!h || !U_host || !R_host) return mc_fail(MC_EINVAL, "null argument");
+  if (h->ng) return mc_fail(MC_EINVAL, "partitioned operator: use the device entry points");
+  if (int rc = user_staging(h, true)) return rc;
+  const int64_t nblk = (h->ne + h->ng) * h->stride;
+  const size_t ubytes = sizeof(double) * size_t(h->n_user_rows) * h->ops->neq * h->ops->np;
+  DG_TRY(cudaMemcpyAsync(h->d_user, U_host, ubytes, cudaMemcpyHostToDevice, h->stream));
+  if (int rc = mc_dg_user_to_internal(h, h->d_user, h->d_host_U, h->stream)) return rc;
+  if (int rc = mc_dg_rhs(h, h->d_host_U, h->d_host_U + 2 * nblk, strategy, h->stream)) return rc;
+  DG_TRY(cudaMemsetAsync(h->d_user_R, 0, ubytes, h->stream));
+  if (int rc = mc_dg_internal_to_user(h, h->d_host_U + 2 * nblk, h->d_user_R, h->stream)) return rc;
+  DG_TRY(cudaMemcpyAsync(R_host, h->d_user_R, ubytes, cudaMemcpyDeviceToHost, h->stream));
   DG_TRY(cudaStreamSynchronize(h->stream));
   return MC_OK;
 }

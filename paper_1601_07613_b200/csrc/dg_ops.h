@@ -18,7 +18,7 @@ struct Ops {
   cudaError_t (*volume)(const View&, const double* U, double* R, int grid, cudaStream_t s);
   cudaError_t (*uncolored)(const View&, const double* U, double* out, bool atomic, int grid,
                            cudaStream_t s);
-  cudaError_t (*gather)(const View&, const double* buf, double* R, cudaStream_t s);
+  cudaError_t (*gather)(const View&, const double* buf, double* R, int cap, cudaStream_t s);
   cudaError_t (*init)(Ops* self);   // occupancy queries, smem opt-in
   int stable_size;                  // doubles of the padded table layout
   cudaError_t (*stage_global)(const double* tables, double* out, cudaStream_t s);
@@ -81,10 +81,12 @@ struct Instance {
     }
     return cudaGetLastError();
   }
-  static cudaError_t gather(const View& v, const double* buf, double* R, cudaStream_t s) {
+  static cudaError_t gather(const View& v, const double* buf, double* R, int cap,
+                            cudaStream_t s) {
     const int64_t total = v.n_elements * C::NEQ * C::NP;
     int64_t g = (total + kThreads - 1) / kThreads;
     if (g > 148 * 16) g = 148 * 16;
+    if (cap > 0 && g > cap) g = cap;
     if (g < 1) g = 1;
     k_gather<C><<<int(g), kThreads, 0, s>>>(v, buf, R);
     return cudaGetLastError();

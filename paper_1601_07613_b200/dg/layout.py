@@ -326,7 +326,10 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
         # the rest of the first color can run while the ghosts are exchanged
         key2 = (code & 0xFFF) if code_sort else np.zeros(len(sid), dtype=np.int64)
         if code_sort and code_sort_window > 0:
-            key2 = key2 + (np.arange(len(sid), dtype=np.int64) // code_sort_window) * 4096
+            # windows counted from each color's first surface (col is
+            # non-decreasing here), so no color starts with a partial window
+            pos = np.arange(len(sid), dtype=np.int64) - np.searchsorted(col, col, side="left")
+            key2 = key2 + (pos // code_sort_window) * 4096
         if code_sort and code_sort_skip_first:
             key2 = np.where(col == 1, 0, key2)
         perm = np.lexsort((np.arange(len(sid)), key2, ghost_r.astype(np.int64), col))

@@ -41,6 +41,34 @@ _STRATEGY = {"colored": 0, "buffered": 1, "atomic": 2}
 _TET_CODE_SORT = 4096
 
 
+def _sort_options(code_sort, kind) -> dict:
+    """Surface order inside each color (any order is race free and keeps
+    every element's accumulation order).  ``code_sort``: False / 0 = keep
+    the layout order; True / 1 = sort every color by side codes (warps read
+    the same face-table rows); an int n >= 2 = sort colors >= 2 inside
+    windows of n surfaces counted from the color's first surface (color 1
+    stays coalesced).  None = the measured default per element kind
+    (whole-color sort +2 % on quads, windows of 4096 on tets,
+    unsorted on triangles), overridable with MC_CODE_SORT."""
+    if code_sort is None:
+        env = os.environ.get("MC_CODE_SORT")
+        if env is not None:
+            try:
+                code_sort = int(env)
+            except ValueError:
+                raise ValueError(f"MC_CODE_SORT must be an integer (0, 1 or a window >= 2), "
+                                 f"got {env!r}") from None
+        else:
+            code_sort = {ElementKind.QUAD: True,
+                         ElementKind.TET: _TET_CODE_SORT}.get(kind, False)
+    if isinstance(code_sort, (bool, np.bool_)) or code_sort in (0, 1):
+        return dict(code_sort=bool(code_sort))
+    n = int(code_sort)
+    if n < 0:
+        raise ValueError(f"code_sort window must be >= 2, got {n}")
+    return dict(code_sort=True, code_sort_window=n, code_sort_skip_first=True)
+
+
 def default_freestream(dim: int, gamma: float = 1.4):
     rho, p = 1.0, 1.0
     vel = (0.3, 0.2, 0.1)[:dim]
@@ -125,31 +153,14 @@ class DGOperator:
     def __init__(self, mesh, coloring: SurfaceColoring | None = None, degree: int = 1,
                  physics: str = "euler", *, period=None, gamma: float = 1.4,
                  velocity=(1.0, 0.5, 0.25), farfield=None, ordering: str | None = None,
-                 world: int = 1, rank: int = 0, code_sort: bool | int | None = None):
+                 world: int = 1, rank: int = 0, code_sort: bool | int | None = None,
+                 grid_cap: int | None = None):
         mortars = None
         if isinstance(mesh, RefinedMesh):
             mortars = mesh.hanging_array()
             mesh = mesh.mesh
         self.mesh = mesh
-        if code_sort is None:
-            # measured: whole-color sort +2 % on quads (c3) and
-            # -4 % on shuffled triangles (c2, loses coalescing) and tets (c4);
-            # windowed sort on tets: see _TET_CODE_SORT.  MC_CODE_SORT=0/1/<window>
-            # overrides
-            env = os.environ.get("MC_CODE_SORT")
-            if env is not None:
-                code_sort = True if env == "1" else int(env)
-            else:
-                code_sort = {ElementKind.QUAD: True,
-                             ElementKind.TET: _TET_CODE_SORT}.get(mesh_kind(mesh), False)
-        # True: sort every color by side codes; an int n >= 2: sort inside
-        # windows of n surfaces, colors >= 2 only (color 1 stays coalesced)
-        if code_sort is True or code_sort is False:
-            self._sort = dict(code_sort=code_sort)
-        else:
-            n = int(code_sort)
-            self._sort = dict(code_sort=n > 1, code_sort_window=max(n, 0),
-                              code_sort_skip_first=True)
+        self._sort = _sort_options(code_sort, mesh_kind(mesh))
         if coloring is None:
             coloring, _ = color(mesh)
         self.coloring = coloring
@@ -200,6 +211,9 @@ class DGOperator:
         self.tables = reference_tables(self.kind, self.degree)
         self.n_basis = self.tables.n_basis
         self._create()
+        self._set_user_rows()
+        if grid_cap is not None:
+            self.set_grid_cap(grid_cap)
         self.halo = None
         if self.part is not None:
             from ..partition import HaloExchange
@@ -247,6 +261,45 @@ class DGOperator:
         self._lib = lib
         self._h = h
         self.stride = int(lib.mc_dg_block_stride(h))
+
+    def _set_user_rows(self):
+        """Tell the library where each internal owned row lives in the
+        caller's (user) element order, for the user-layout entry points.
+        Single domain: the whole state in user order.  Partitioned: this
+        rank's owned elements in ascending user id (``user_rows``)."""
+        ids = self.owned_user_ids()
+        if self.part is None:
+            src, n = ids, self.mesh.n_elements
+        else:
+            src, n = np.searchsorted(np.sort(ids), ids), len(ids)
+        src = np.ascontiguousarray(src, dtype=np.int64)
+        _native.check(self._lib.mc_dg_set_user_rows(self._h, _native.ptr(src), int(n)))
+
+    def user_rows(self, U: np.ndarray) -> np.ndarray:
+        """The caller-order rows this operator's user-layout entry points
+        take: the whole state, or (partitioned) this rank's owned elements
+        in ascending user id, as (rows, N_eq * N_p)."""
+        U = np.asarray(U, dtype=np.float64).reshape(self.mesh.n_elements, -1)
+        if self.part is None:
+            return np.ascontiguousarray(U)
+        return np.ascontiguousarray(U[np.sort(self.owned_user_ids())])
+
+    def user_to_device(self, user_dev, U_dev, stream=None) -> None:
+        """Device permutation: caller-order rows -> internal blocks."""
+        _native.check(self._lib.mc_dg_user_to_internal(self._h, _native.ptr(user_dev),
+                                                        _native.ptr(U_dev),
+                                                        _native.stream_ptr(stream)))
+
+    def device_to_user(self, U_dev, user_dev, stream=None) -> None:
+        """Device permutation: internal blocks -> caller-order rows."""
+        _native.check(self._lib.mc_dg_internal_to_user(self._h, _native.ptr(U_dev),
+                                                        _native.ptr(user_dev),
+                                                        _native.stream_ptr(stream)))
+
+    def set_grid_cap(self, max_blocks: int) -> None:
+        """Cap every persistent-grid launch at ``max_blocks`` blocks (0 =
+        the occupancy-sized default), so each warp loops over many tiles."""
+        _native.check(self._lib.mc_dg_set_grid_cap(self._h, int(max_blocks)))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -345,11 +398,17 @@ class DGOperator:
         overlapped: post the exchange, run the part of color 1 that touches
         no ghost, complete the exchange, then the rest of color 1 and the
         other colors."""
-        h = self.halo.start(U_dev) if self.halo is not None else None
-        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, stream, part="inner")
+        import torch
+        cs = stream if stream is not None else torch.cuda.current_stream()
+        # halo gather / ghost writes on the compute stream, ordered after the
+        # previous stage's last-touch updates and before the interface pass
+        with torch.cuda.stream(cs):
+            h = self.halo.start(U_dev) if self.halo is not None else None
+        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, cs, part="inner")
         if h is not None:
-            self.halo.finish(U_dev, h)
-        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, stream, part="interface")
+            with torch.cuda.stream(cs):
+                self.halo.finish(U_dev, h)
+        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, cs, part="interface")
         for c in range(2, self.n_colors + 1):
             self.color_pass_device(c, U_dev, U0_dev, R_dev, mode, a, b, dt, stream)
 
@@ -373,18 +432,49 @@ class DGOperator:
         _native.check(self._lib.mc_dg_ssprk3(self._h, _native.ptr(U_dev), _native.ptr(work_dev),
                                              float(dt), int(steps), _native.stream_ptr(stream)))
 
-    def rhs(self, U: np.ndarray, strategy: str = "colored") -> np.ndarray:
-        import torch
-        Ud = self.to_device(U)
-        Rd = torch.zeros_like(Ud)
-        self.rhs_device(Ud, Rd, strategy)
-        return self.from_device(Rd)
+    def _user_array(self, U) -> np.ndarray:
+        U = np.asarray(U, dtype=np.float64)
+        if U.size != self.mesh.n_elements * self.block_width():
+            raise ValueError(f"state must have shape ({self.mesh.n_elements}, "
+                             f"{self.n_equations}, {self.n_basis})")
+        return np.ascontiguousarray(U).reshape(self.mesh.n_elements, self.n_equations,
+                                               self.n_basis)
 
-    def ssprk3(self, U: np.ndarray, dt: float, steps: int = 1) -> np.ndarray:
-        """End to end through host buffers (``mc_dg_ssprk3_host``)."""
-        B = np.ascontiguousarray(self.to_internal(U))
-        _native.check(self._lib.mc_dg_ssprk3_host(self._h, _native.ptr(B), float(dt), int(steps)))
-        return self.from_internal(B)
+    def rhs(self, U: np.ndarray, strategy: str = "colored", out: np.ndarray | None = None
+            ) -> np.ndarray:
+        """Eq. (2) residual of a host state in the caller's element order,
+        end to end (``mc_dg_rhs_user_host``: H2D, device permutation into
+        the color-major layout, the strategy's launches, permutation back,
+        D2H)."""
+        if self.part is not None:
+            raise ValueError("partitioned operator: use rhs_device / stage_distributed")
+        U = self._user_array(U)
+        R = np.empty_like(U) if out is None else out
+        if R.shape != U.shape or R.dtype != np.float64 or not R.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 array shaped like U")
+        _native.check(self._lib.mc_dg_rhs_user_host(self._h, _native.ptr(U), _native.ptr(R),
+                                                    _STRATEGY[strategy]))
+        return R
+
+    def ssprk3(self, U: np.ndarray, dt: float, steps: int = 1, inplace: bool = False
+               ) -> np.ndarray:
+        """``steps`` SSP-RK3 steps of a host state in the caller's element
+        order, end to end (``mc_dg_ssprk3_user_host``: H2D, device
+        permutation, the fused colored launches replayed as one CUDA graph
+        per step, permutation back, D2H).  ``inplace=True`` updates a
+        C-contiguous float64 ``U`` (e.g. in pinned memory) and returns it."""
+        if self.part is not None:
+            raise ValueError("partitioned operator: use ssprk3_distributed")
+        if inplace:
+            if not (isinstance(U, np.ndarray) and U.dtype == np.float64 and U.flags.c_contiguous
+                    and U.size == self.mesh.n_elements * self.block_width()):
+                raise ValueError("inplace needs a C-contiguous float64 array of the state size")
+            B = U
+        else:
+            B = self._user_array(U).copy()
+        _native.check(self._lib.mc_dg_ssprk3_user_host(self._h, _native.ptr(B), float(dt),
+                                                       int(steps)))
+        return B
 
     def ssprk3_host_internal(self, B: np.ndarray, dt: float, steps: int = 1) -> None:
         """In-place SSP-RK3 on a host array already in the internal layout

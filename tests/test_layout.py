@@ -30,8 +30,7 @@ def test_code_sort_windows_permute_within_colors():
         if kw.get("code_sort_skip_first"):
             assert np.array_equal(sl.mesh_surface[b[0]:b[1]], base.mesh_surface[b[0]:b[1]])
             key = sl.code.astype(np.int64) & 0xFFF
-            for s0 in range(0, int(b[-1]), win):       # windows of the global order
-                w = np.arange(s0, min(s0 + win, int(b[-1])))
-                for c in range(1, col.n_colors):      # windows never cross a color
-                    m = w[(w >= b[c]) & (w < b[c + 1])]
+            for c in range(1, col.n_colors):          # windows start at each color
+                for s0 in range(int(b[c]), int(b[c + 1]), win):
+                    m = np.arange(s0, min(s0 + win, int(b[c + 1])))
                     assert (np.diff(key[m]) >= 0).all()

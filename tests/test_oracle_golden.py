@@ -5,7 +5,53 @@ import numpy as np
 import pytest
 
 from conftest import AMR_CASES, MESH_CASES, load_golden, manifest
-from oracle import amr_oracle, coloring_oracle, plan_oracle, sweeps_oracle
+from oracle import amr_oracle, coloring_oracle, mesh_oracle, plan_oracle, sweeps_oracle
+
+MO = mesh_oracle
+ORACLE_MESHES = {
+    "tri_6x5": lambda: MO.gen_tri_rect(6, 5),
+    "tri_8x8": lambda: MO.gen_tri_rect(8, 8),
+    "tri_8x8_per": lambda: MO.gen_tri_rect(8, 8, (True, True)),
+    "tri_6x6_per": lambda: MO.gen_tri_rect(6, 6, (True, True)),
+    "tri_64x64": lambda: MO.gen_tri_rect(64, 64),
+    "shuf_tri_64": lambda: MO.shuffle_elements(MO.gen_tri_rect(64, 64), 0),
+    "shuf_tri_16": lambda: MO.shuffle_elements(MO.gen_tri_rect(16, 16), 0),
+    "quad_5x5": lambda: MO.gen_quad_rect(5, 5),
+    "quad_16x16": lambda: MO.gen_quad_rect(16, 16),
+    "quad_4x4_per": lambda: MO.gen_quad_rect(4, 4, (True, True)),
+    "tet_2x2x2": lambda: MO.gen_tet_prism(2, 2, 2),
+    "tet_4x4x4": lambda: MO.gen_tet_prism(4, 4, 4),
+    "shuf_tet_3": lambda: MO.shuffle_elements(MO.gen_tet_prism(3, 3, 3), 5),
+}
+
+
+@pytest.mark.parametrize("name", sorted(ORACLE_MESHES))
+def test_mesh_oracle_matches_reference(name):
+    g = load_golden(name)
+    m = ORACLE_MESHES[name]()
+    for k in ("vertices", "elem_kind", "elem_verts", "elem_surfs", "surf_verts", "surf_elems"):
+        assert np.array_equal(m[k], g["mesh_" + k]), k
+
+
+def test_mesh_oracle_c2_fingerprint():
+    """c2 at full size against the reference's config-scale CRCs."""
+    import json
+    import zlib
+    from conftest import GOLDEN
+    want = json.loads((GOLDEN / "config" / "c2.json").read_text())["mesh"]
+    m = MO.shuffle_elements(MO.gen_tri_rect(708, 708), 0)
+    for k in ("elem_verts", "elem_surfs", "surf_verts", "surf_elems"):
+        assert zlib.crc32(np.ascontiguousarray(m[k]).astype("<i8").tobytes()) == want["crc_" + k]
+
+
+@pytest.mark.parametrize("name", ["tri_64x64", "shuf_tet_3", "quad_16x16"])
+def test_threaded_colored_sweep_oracle(name):
+    g = load_golden(name)
+    ne = len(g["mesh_elem_kind"])
+    for workers in (1, 3, 8):
+        tot = sweeps_oracle.sweep_colored_threads(g["mesh_surf_elems"], ne, g["payload_s0"],
+                                                  g["colors"], int(g["n_colors"]), workers)
+        assert np.array_equal(tot, g["totals_s0"])
 
 
 @pytest.mark.parametrize("name", MESH_CASES)
