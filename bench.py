@@ -415,15 +415,10 @@ def main():
                     mark(events, mode, a, c)
                     op.color_pass_device(c, U, U0, R, mode, a, b, dt, stream)
                 continue
-            # ghost exchange overlapped with the ghost-free part of color 1
-            h = op.halo.start(U)
-            mark(events, mode, a, 1)
-            op.color_pass_device(1, U, U0, R, mode, a, b, dt, stream, part="inner")
-            op.halo.finish(U, h)
-            op.color_pass_device(1, U, U0, R, mode, a, b, dt, stream, part="interface")
-            for c in range(2, nc + 1):
-                mark(events, mode, a, c)
-                op.color_pass_device(c, U, U0, R, mode, a, b, dt, stream)
+            # ghost exchange overlapped with the ghost-free part of color 1;
+            # the send rows were packed by the previous stage's last touches
+            op.stage_distributed(U, U0, R, mode, a, b, dt, stream,
+                                 marker=lambda c, m=mode, aa=a: mark(events, m, aa, c))
 
     def barrier():
         if world > 1:

@@ -229,6 +229,14 @@ int mc_dg_color_pass(mc_dg* dg, int color, double* U_dev, double* U0_dev,
 int mc_dg_color_range_pass(mc_dg* dg, int color, int64_t begin, int64_t end,
                            double* U_dev, double* U0_dev, double* R_dev, int rk_mode,
                            double a, double b, double dt, void* stream);
+/* Partitioned runs: slot[e] (n_elements entries, -1 = none) names the row of
+ * the caller's ghost-exchange send buffer (n_slots blocks of `stride`
+ * doubles, device memory) that owned element e is sent from.  Every
+ * last-touch pass of an RK stage then also stores e's updated block there,
+ * so the next stage's exchange posts the buffer without a gather.  slot =
+ * NULL turns it off. */
+int mc_dg_set_send_rows(mc_dg* dg, const int32_t* slot_host, double* send_buf_dev,
+                        int64_t n_slots);
 /* n_steps SSP-RK3 steps; work_dev = 2 blocks arrays (U0, R scratch). */
 int mc_dg_ssprk3(mc_dg* dg, double* U_dev, double* work_dev, double dt,
                  int n_steps, void* stream);

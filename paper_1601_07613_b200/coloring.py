@@ -190,25 +190,24 @@ def naive_greedy(mesh: Mesh) -> SurfaceColoring:
 
 def verify_coloring(mesh: Mesh, coloring: SurfaceColoring) -> list:
     """Every element with a repeated color and every uncolored surface;
-    empty means complete and valid (coloring.py:491-522)."""
+    empty means complete and valid (same diagnostics, in the same order and
+    wording, as coloring.py:491-522).  A slot is in conflict when another
+    slot of its element row carries the same color (>= 1); the slot-pair
+    comparison over the <= 4 local sides is done for all elements at once."""
     colors = np.asarray(coloring.colors)
     es = mesh.elem_surfs
-    has = es >= 0
-    per_elem = np.where(has, colors[np.where(has, es, 0)], -2).astype(np.int64)
-    per_elem = np.where(per_elem >= 1, per_elem, -2)
-    srt = np.sort(per_elem, axis=1)
-    rep = ((srt[:, 1:] == srt[:, :-1]) & (srt[:, 1:] >= 1)).any(axis=1)
+    slot_col = np.where(es >= 0, colors[np.maximum(es, 0)], 0).astype(np.int64)
+    slot_col[slot_col < 1] = 0                       # uncolored / absent: never a repeat
+    twin = (slot_col[:, :, None] == slot_col[:, None, :]) & (slot_col[:, :, None] > 0)
+    in_conflict = twin.sum(axis=2) > 1               # (ne, sides)
     out: list = []
-    for e in np.flatnonzero(rep):
-        row = per_elem[e]
-        vals, cnt = np.unique(row[row >= 1], return_counts=True)
-        repeated = [int(v) for v in vals[cnt > 1]]
-        sids = [int(s) for s in es[e] if s >= 0 and int(colors[s]) in repeated]
+    for e in np.flatnonzero(in_conflict.any(axis=1)):
+        hit = in_conflict[e]
         out.append(Diagnostic(
             "conflict",
-            f"element {e} repeats color(s) {repeated} on surfaces {sids}",
+            f"element {e} repeats color(s) {sorted(set(slot_col[e][hit].tolist()))} "
+            f"on surfaces {es[e][hit].tolist()}",
             element_id=int(e)))
-    for k in np.flatnonzero(colors < 1):
-        out.append(Diagnostic("uncolored", f"surface {k} has no color",
-                              surface_id=int(k)))
+    out.extend(Diagnostic("uncolored", f"surface {k} has no color", surface_id=int(k))
+               for k in np.flatnonzero(colors < 1))
     return out

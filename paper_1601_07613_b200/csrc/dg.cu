@@ -43,6 +43,7 @@ struct mc_dg {
   int64_t n_user_rows = 0;
   double* d_user = nullptr;        // user-layout staging (n_user_rows x W)
   double* d_user_R = nullptr;      // user-layout residual staging
+  int32_t* d_send_slot = nullptr;  // per owned element: ghost send-buffer slot or -1
 };
 
 namespace {
@@ -110,6 +111,75 @@ __global__ void k_internal_to_user(const double* __restrict__ U, const int64_t* 
 int copy_grid(int64_t total) {
   const int64_t g = (total + 255) / 256;
   return int(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
+}
+
+// Tables of the projection through P_{p-1} (dg_kernels.cuh Cfg::NPL):
+// WPSI[q][m] = w_q phi_m(q) and D_r[j][m] with dphi_r[q][j] =
+// sum_m D_r[j][m] phi_m(q), fitted by least squares on the volume points
+// (the representation is exact: the fit residual is rounding).  Also checks
+// the hierarchical mode order the kernels' sparsity relies on.
+int p1_tables(const Ops* ops, const mc_dg_desc* d, double* out) {
+  const int M = ops->npl, nq = ops->nqv, np = ops->np, dim = ops->dim;
+  double* wpsi = out;
+  double* dmat = out + nq * M;
+  for (int q = 0; q < nq; ++q)
+    for (int m = 0; m < M; ++m) wpsi[q * M + m] = d->vol_w[q] * d->vol_phi[q * np + m];
+  // normal equations A^T A x = A^T b, A = phi[:, :M] (long double Gauss-Jordan)
+  std::vector<long double> ata(M * M, 0.0L), inv(M * M, 0.0L);
+  for (int a = 0; a < M; ++a)
+    for (int b = 0; b < M; ++b)
+      for (int q = 0; q < nq; ++q)
+        ata[a * M + b] += (long double)d->vol_phi[q * np + a] * d->vol_phi[q * np + b];
+  for (int a = 0; a < M; ++a) inv[a * M + a] = 1.0L;
+  for (int c = 0; c < M; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < M; ++r)
+      if (std::fabs((double)ata[r * M + c]) > std::fabs((double)ata[piv * M + c])) piv = r;
+    if (std::fabs((double)ata[piv * M + c]) < 1e-12)
+      return mc_fail(MC_EINVAL, "volume points do not determine the P_{p-1} modes");
+    for (int k = 0; k < M; ++k) {
+      std::swap(ata[c * M + k], ata[piv * M + k]);
+      std::swap(inv[c * M + k], inv[piv * M + k]);
+    }
+    const long double f = 1.0L / ata[c * M + c];
+    for (int k = 0; k < M; ++k) {
+      ata[c * M + k] *= f;
+      inv[c * M + k] *= f;
+    }
+    for (int r = 0; r < M; ++r)
+      if (r != c) {
+        const long double g = ata[r * M + c];
+        for (int k = 0; k < M; ++k) {
+          ata[r * M + k] -= g * ata[c * M + k];
+          inv[r * M + k] -= g * inv[c * M + k];
+        }
+      }
+  }
+  // shell of mode j: number of P_{deg(j)-1} modes (0 for the constant)
+  auto nsimp = [&](int deg) {
+    if (deg < 0) return 0;
+    return dim == 2 ? (deg + 1) * (deg + 2) / 2 : (deg + 1) * (deg + 2) * (deg + 3) / 6;
+  };
+  for (int r = 0; r < dim; ++r)
+    for (int j = 0; j < np; ++j) {
+      std::vector<long double> atb(M, 0.0L);
+      for (int m = 0; m < M; ++m)
+        for (int q = 0; q < nq; ++q)
+          atb[m] += (long double)d->vol_phi[q * np + m] * d->vol_dphi[(r * nq + q) * np + j];
+      int deg = 0;
+      while (j >= nsimp(deg)) ++deg;
+      const int shell = nsimp(deg - 1);
+      double resid = 0.0;
+      for (int m = 0; m < M; ++m) {
+        long double x = 0.0L;
+        for (int k = 0; k < M; ++k) x += inv[m * M + k] * atb[k];
+        dmat[(r * np + j) * M + m] = double(x);
+        if (m >= shell) resid = std::max(resid, std::fabs(double(x)));
+      }
+      if (ops->p1proj && resid > 1e-9)
+        return mc_fail(MC_EINVAL, "basis modes are not ordered by total degree");
+    }
+  return MC_OK;
 }
 
 int colored_pass(mc_dg* h, double* U, double* R, const mcdg::RK* rk, cudaStream_t s) {
@@ -196,6 +266,11 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
     std::memcpy(t, d->vol_dphi, sizeof(double) * dim * ops->nqv * ops->np);
     t += dim * ops->nqv * ops->np;
     std::memcpy(t, d->vol_w, sizeof(double) * ops->nqv);
+    t += ops->nqv;
+    if (int rc = p1_tables(ops, d, t)) {
+      delete h;
+      return rc;
+    }
   }
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&h->d_left, d->surf_left, h->ns);
@@ -255,6 +330,7 @@ MC_API int mc_dg_destroy(mc_dg* h) {
   cudaFree(h->d_user_src);
   cudaFree(h->d_user);
   cudaFree(h->d_user_R);
+  cudaFree(h->d_send_slot);
   if (h->step_exec) cudaGraphExecDestroy(h->step_exec);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -422,6 +498,28 @@ MC_API int mc_dg_set_user_rows(mc_dg* h, const int64_t* src, int64_t n_user_rows
   h->n_user_rows = 0;
   DG_TRY(upload(&h->d_user_src, src, h->ne));
   h->n_user_rows = n_user_rows;
+  return MC_OK;
+}
+
+MC_API int mc_dg_set_send_rows(mc_dg* h, const int32_t* slot, double* send_buf_dev,
+                                int64_t n_slots) {
+  if (!h) return mc_fail(MC_EINVAL, "null argument");
+  cudaFree(h->d_send_slot);
+  h->d_send_slot = nullptr;
+  h->view.send_slot = nullptr;
+  h->view.send_buf = nullptr;
+  if (h->step_exec) {   // the captured step baked the old view in
+    cudaGraphExecDestroy(h->step_exec);
+    h->step_exec = nullptr;
+  }
+  if (!slot) return MC_OK;
+  if (!send_buf_dev) return mc_fail(MC_EINVAL, "send buffer missing");
+  for (int64_t e = 0; e < h->ne; ++e)
+    if (slot[e] < -1 || slot[e] >= n_slots)
+      return mc_fail(MC_EINVAL, "send slot out of range");
+  DG_TRY(upload(&h->d_send_slot, slot, h->ne));
+  h->view.send_slot = h->d_send_slot;
+  h->view.send_buf = send_buf_dev;
   return MC_OK;
 }
 

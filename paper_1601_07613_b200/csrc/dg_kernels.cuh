@@ -80,7 +80,22 @@ struct Cfg {
   static constexpr int T_VPHI = T_FW + NQF;
   static constexpr int T_VDPHI = T_VPHI + NQV * NP;
   static constexpr int T_VW = T_VDPHI + DIM * NQV * NP;
-  static constexpr int T_SIZE = T_VW + NQV;
+  // Projection through P_{p-1} (simplices, register kernels): the reference
+  // gradients of the P_p modes lie in P_{p-1} (NPL modes), so
+  //   sum_q w_q dphi_r[q][j] G[q] = sum_m D_r[j][m] (sum_q w_q phi_m[q] G[q]).
+  // Tables (computed at operator creation from vol_phi / vol_dphi):
+  // WPSI[q][m] = w_q phi_m(q), DMAT[r][j][m]; modes are ordered by total
+  // degree, so D_r[j][m] = 0 unless m < NPL(deg(j) - 1).
+  static constexpr int NPL = (K == QUAD || NEQ * NP > 64) ? 1
+                           : (K == TRI) ? P * (P + 1) / 2 : P * (P + 1) * (P + 2) / 6;
+#ifdef MC_NO_P1PROJ
+  static constexpr bool P1PROJ = false;
+#else
+  static constexpr bool P1PROJ = (K != QUAD) && P >= 1 && NEQ * NP <= 64;
+#endif
+  static constexpr int T_WPSI = T_VW + NQV;
+  static constexpr int T_DMAT = T_WPSI + NQV * NPL;
+  static constexpr int T_SIZE = T_DMAT + DIM * NP * NPL;
   // shared-memory copy: rows padded to an even length so that pairs of
   // basis values are one 16-byte broadcast load (LDS.128)
   static constexpr int NPP = (NP + 1) & ~1;
@@ -89,7 +104,9 @@ struct Cfg {
   static constexpr int S_VPHI = S_FW + ((NQF + 1) & ~1);
   static constexpr int S_VDPHI = S_VPHI + NQV * NPP;
   static constexpr int S_VW = S_VDPHI + DIM * NQV * NPP;
-  static constexpr int S_SIZE = S_VW + ((NQV + 1) & ~1);
+  static constexpr int S_WPSI = S_VW + ((NQV + 1) & ~1);
+  static constexpr int S_DMAT = S_WPSI + ((NQV * NPL + 1) & ~1);
+  static constexpr int S_SIZE = S_DMAT + ((DIM * NP * NPL + 1) & ~1);
   // per-warp scratch (doubles) for the surface kernels.  Every array is
   // indexed so that the lane-parallel accesses (one lane per task or per
   // (slot, eq)) step by an ODD number of doubles: conflict-free banks.
@@ -196,6 +213,11 @@ struct View {
   int64_t n_surfaces;
   int64_t stride;      // doubles per element block
   Params prm;
+  // partitioned runs: the last-touch pass of an RK stage also writes each
+  // interface element's new block into its slot of the ghost-exchange send
+  // buffer (send_slot[e] >= 0), so the next stage posts it without a pack
+  const int32_t* send_slot;
+  double* send_buf;
 };
 
 struct RK {
@@ -428,9 +450,15 @@ __device__ __forceinline__ void stage_tables(const double* __restrict__ g, doubl
     } else if (i < C::S_VW) {
       const int row = (i - C::S_VPHI) / C::NPP, j = (i - C::S_VPHI) - row * C::NPP;
       if (j < C::NP) v = __ldg(g + C::T_VPHI + row * C::NP + j);  // vphi and vdphi rows
-    } else {
+    } else if (i < C::S_WPSI) {
       const int k = i - C::S_VW;
       if (k < C::NQV) v = __ldg(g + C::T_VW + k);
+    } else if (i < C::S_DMAT) {
+      const int k = i - C::S_WPSI;
+      if (k < C::NQV * C::NPL) v = __ldg(g + C::T_WPSI + k);
+    } else {
+      const int k = i - C::S_DMAT;
+      if (k < C::DIM * C::NP * C::NPL) v = __ldg(g + C::T_DMAT + k);
     }
     s[i] = v;
   }
@@ -796,6 +824,10 @@ k_surface_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk,
           for (int j = 0; j < C::NP; ++j) acc[j] = rk.b * fma(rk.dt, acc[j], u[j]);
         }
         store_run<C::NP>(U + off, acc);
+        if (v.send_slot) {
+          const int sl = __ldg(v.send_slot + c.e);
+          if (sl >= 0) store_run<C::NP>(v.send_buf + int64_t(sl) * v.stride + ln.eq * C::NP, acc);
+        }
       } else {
         store_run<C::NP>(R + off, acc);
       }

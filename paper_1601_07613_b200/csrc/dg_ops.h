@@ -25,6 +25,8 @@ struct Ops {
   // copy the volume part of the padded tables into this configuration's
   // constant-memory array (c_voltab)
   cudaError_t (*upload_const)(const double* ptables_dev);
+  int npl;                          // P_{p-1} modes of the factored projection
+  int p1proj;                       // the register kernels use it (Cfg::P1PROJ)
 };
 
 // defined in dg_tri.cu / dg_quad.cu / dg_tet.cu; nullptr if not compiled
@@ -147,7 +149,7 @@ struct Instance {
     static Ops o{C::DIM, C::NEQ, C::NP, C::NQF, C::NQV, C::NCODES, C::T_SIZE,
                  T::OK ? T::THREADS : C::THREADS, T::OK ? T::SW : C::SPW,
                  0, 0, 0, &colored, &volume, &uncolored, &gather, &init, C::S_TOTAL,
-                 &stage_global, &upload_const};
+                 &stage_global, &upload_const, C::NPL, C::P1PROJ ? 1 : 0};
     return &o;
   }
 };

@@ -164,6 +164,118 @@ template <int H> constexpr int kVolUnroll = MC_VOL_UNROLL;
 template <int H> constexpr int kVolUnroll = H == 2 ? 2 : 1;
 #endif
 
+#ifdef MC_P1PROJ_H1
+constexpr bool kP1ProjH1 = true;
+#else
+constexpr bool kP1ProjH1 = false;
+#endif
+
+// Modes of P_d on the simplex (d < 0: none) and the P_{p-1} modes the
+// reference gradient of mode j needs (modes are ordered by total degree).
+template <int K>
+constexpr int simplex_modes(int d) {
+  return d < 0 ? 0 : (K == TRI ? (d + 1) * (d + 2) / 2 : (d + 1) * (d + 2) * (d + 3) / 6);
+}
+template <int K>
+constexpr int grad_shell(int j) {
+  int d = 0;
+  while (j >= simplex_modes<K>(d)) ++d;
+  return simplex_modes<K>(d - 1);
+}
+
+// Volume integral through P_{p-1} (Cfg::P1PROJ, simplices): the contravariant
+// fluxes are first projected onto the NPL modes of P_{p-1} with the weights
+// folded in (Pm[r][k][m] = sum_q w_q phi_m(q) Ft_r(q)[k]), then lifted once
+// per element, acc[k][j] += sum_r sum_m D_r[j][m] Pm[r][k][m] with D's
+// zero blocks skipped at compile time (c4: 3 x 4 instead of 3 x 10
+// multiply-adds per point and equation).  Two lanes per side additionally
+// split the volume points: at each point pair, lane h evaluates the flux of
+// point 2i+h only (the traces and the fluxes of the other lane's equations
+// cross by shuffles), so every flux is evaluated once, not twice.
+template <class C, int PH>
+__device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (&u)[Tpe<C>::WH],
+                                              const double (&ji)[C::DIM * C::DIM], int h,
+                                              int nown, bool mine, const Params& P,
+                                              double (&acc)[Tpe<C>::WH]) {
+  constexpr int NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH, DIM = C::DIM, M = C::NPL;
+  constexpr int H = Tpe<C>::H, WH = Tpe<C>::WH;
+  const double* wpsi = vphi + (C::S_WPSI - C::S_VPHI);
+  const double* dmat = vphi + (C::S_DMAT - C::S_VPHI);
+  double Pm[DIM][NEQH][M];
+#pragma unroll
+  for (int r = 0; r < DIM; ++r)
+#pragma unroll
+    for (int k = 0; k < NEQH; ++k)
+#pragma unroll
+      for (int m = 0; m < M; ++m) Pm[r][k][m] = 0.0;
+  // whole point on this lane: every own equation's flux at point q
+  auto point = [&](int q) {
+    double own[NEQH], s[NEQ];
+#pragma unroll
+    for (int k = 0; k < NEQH; ++k) own[k] = tdot<NP, WH>(vphi + q * C::NPP, u, k * NP);
+    assemble_state<C>(own, h, s);
+    double Ft[DIM * NEQ];
+    Physics<PH, DIM, NEQ>::vflux(s, ji, P, Ft);
+#pragma unroll
+    for (int r = 0; r < DIM; ++r)
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k) {
+        const double f = (mine && k < nown) ? own_part<C>(Ft + r * NEQ, h, k) : 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) Pm[r][k][m] = fma(wpsi[q * M + m], f, Pm[r][k][m]);
+      }
+  };
+  if constexpr (H == 1) {
+#pragma unroll 1
+    for (int q = 0; q < C::NQV; ++q) point(q);
+  } else {
+    constexpr int NA = Tpe<C>::NA;
+#pragma unroll 1
+    for (int q0 = 0; q0 + 1 < C::NQV; q0 += 2) {
+      const int q1 = q0 + 1;
+      double mt[NEQH], ot[NEQH];
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k) {
+        const double a = tdot<NP, WH>(vphi + q0 * C::NPP, u, k * NP);
+        const double b = tdot<NP, WH>(vphi + q1 * C::NPP, u, k * NP);
+        ot[k] = __shfl_xor_sync(kFull, h ? a : b, 1);    // partner's traces at my point
+        mt[k] = h ? b : a;                                // mine at my point (q0 + h)
+      }
+      double s[NEQ], Ft[DIM * NEQ];
+#pragma unroll
+      for (int e = 0; e < NEQ; ++e)
+        s[e] = (e < NA) ? (h == 0 ? mt[e] : ot[e]) : (h == 1 ? mt[e - NA] : ot[e - NA]);
+      Physics<PH, DIM, NEQ>::vflux(s, ji, P, Ft);
+#pragma unroll
+      for (int r = 0; r < DIM; ++r)
+#pragma unroll
+        for (int k = 0; k < NEQH; ++k) {
+          const double fm = own_part<C>(Ft + r * NEQ, h, k);        // my eq, my point
+          const double fr = __shfl_xor_sync(kFull, own_part<C>(Ft + r * NEQ, h ^ 1, k), 1);
+          const bool on = mine && k < nown;
+          const double f0 = on ? (h ? fr : fm) : 0.0;              // at q0
+          const double f1 = on ? (h ? fm : fr) : 0.0;              // at q1
+#pragma unroll
+          for (int m = 0; m < M; ++m)
+            Pm[r][k][m] = fma(wpsi[q1 * M + m], f1, fma(wpsi[q0 * M + m], f0, Pm[r][k][m]));
+        }
+    }
+    if constexpr (C::NQV % 2) point(C::NQV - 1);
+  }
+#pragma unroll
+  for (int k = 0; k < NEQH; ++k)
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      double a = acc[k * NP + j];
+#pragma unroll
+      for (int r = 0; r < DIM; ++r)
+#pragma unroll
+        for (int m = 0; m < grad_shell<C::KIND>(j); ++m)
+          a = fma(dmat[(r * NP + j) * M + m], Pm[r][k][m], a);
+      acc[k * NP + j] = a;
+    }
+}
+
 // Volume integral of this lane's element (its equations), added into acc.
 template <class C, int PH>
 __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[Tpe<C>::WH],
@@ -241,6 +353,12 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
     return;
   }
 #endif
+  // two lanes per side (tets): c4 first-touch color 4.91 -> 4.57 ms; one
+  // lane (c2 triangles) measured slower (color 1 3.55 -> 3.27 TB/s)
+  if constexpr (C::P1PROJ && (Tpe<C>::H == 2 || kP1ProjH1)) {
+    tpe_volume_p1<C, PH>(vphi, u, ji, h, nown, mine, P, acc);
+    return;
+  }
   constexpr int kUnroll = kVolUnroll<Tpe<C>::H>;
 #pragma unroll kUnroll
   for (int q = 0; q < C::NQV; ++q) {
@@ -805,6 +923,11 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
           for (int j = 0; j < WH; ++j) acc[j] = rk.b * fma(rk.dt, acc[j], u[j]);
         }
         tstore<WH, kWhole, T::V4>(U + off, n, acc);
+        if (v.send_slot) {
+          const int sl = __ldg(v.send_slot + t.e);
+          if (sl >= 0)
+            tstore<WH, kWhole, T::V4>(v.send_buf + int64_t(sl) * v.stride + ln.eq0 * C::NP, n, acc);
+        }
       } else {
         tstore<WH, kWhole, T::V4>(R + off, n, acc);
       }

@@ -218,6 +218,8 @@ class DGOperator:
         if self.part is not None:
             from ..partition import HaloExchange
             self.halo = HaloExchange(self.part, "cuda")
+            if os.environ.get("MC_KERNEL_PACK", "1") != "0":
+                self.halo.attach(self, self.stride)
 
     # ---------------------------------------------------------- native
     def _create(self):
@@ -393,24 +395,32 @@ class DGOperator:
             _native.stream_ptr(stream)))
 
     def stage_distributed(self, U_dev, U0_dev, R_dev, mode: int, a: float, b: float, dt: float,
-                          stream=None) -> None:
+                          stream=None, marker=None) -> None:
         """One SSP-RK stage on a partitioned operator with the ghost exchange
         overlapped: post the exchange, run the part of color 1 that touches
         no ghost, complete the exchange, then the rest of color 1 and the
-        other colors."""
+        other colors.  ``marker(color)`` (optional) is called before each
+        color's first launch (the bench records CUDA events there)."""
         import torch
         cs = stream if stream is not None else torch.cuda.current_stream()
-        # halo gather / ghost writes on the compute stream, ordered after the
-        # previous stage's last-touch updates and before the interface pass
+        # halo work on the compute stream: the send gather (when needed) is
+        # ordered after the previous stage's last-touch updates, the ghost
+        # rows are read only after the transfers complete
         with torch.cuda.stream(cs):
             h = self.halo.start(U_dev) if self.halo is not None else None
+        if marker:
+            marker(1)
         self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, cs, part="inner")
         if h is not None:
             with torch.cuda.stream(cs):
                 self.halo.finish(U_dev, h)
         self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, cs, part="interface")
         for c in range(2, self.n_colors + 1):
-            self.color_pass_device(c, U_dev, U0_dev, R_dev, mode, a, b, dt, stream)
+            if marker:
+                marker(c)
+            self.color_pass_device(c, U_dev, U0_dev, R_dev, mode, a, b, dt, cs)
+        if self.halo is not None:
+            self.halo.stage_done(rk=mode != 0)
 
     def work_device(self):
         import torch

@@ -117,42 +117,92 @@ def build_partition(mesh: Mesh, colors, n_colors: int, owner: np.ndarray,
 
 class HaloExchange:
     """Grouped point-to-point ghost exchange of element blocks (rows of a
-    (n_local, stride) tensor) with ``torch.distributed``."""
+    (n_local, stride) tensor) with ``torch.distributed``.
+
+    Sends go out of one persistent buffer, the owned interface rows grouped
+    by peer (each peer's rows in its ghost order); receives land directly in
+    the ghost rows of U (contiguous per peer), so nothing is copied after
+    the transfer.  With ``attach(op)`` the operator's last-touch passes
+    write every interface element's updated block into its send-buffer row
+    (``mc_dg_set_send_rows``), so a stage that follows an RK stage posts the
+    buffer as is; otherwise ``start`` gathers it first."""
 
     def __init__(self, part: Partition, device):
         import torch
         self.part = part
         self.device = device
-        self.send_idx = {q: torch.as_tensor(ix, dtype=torch.int64, device=device)
-                         for q, ix in part.send.items()}
+        self.peers = sorted(part.send)
+        self.offs, n = {}, 0
+        for q in self.peers:
+            self.offs[q] = (n, n + len(part.send[q]))
+            n += len(part.send[q])
+        rows = (np.concatenate([part.send[q] for q in self.peers]) if self.peers
+                else np.zeros(0, dtype=np.int64))
+        self.rows = rows
+        self.n_send = n
+        self.send_idx = torch.as_tensor(rows, dtype=torch.int64, device=device)
+        self.send_buf = None
+        self.packed_by_kernel = False
+        self.fresh = False
+
+    def _buffer(self, U):
+        import torch
+        if self.send_buf is None or self.send_buf.shape[1:] != U.shape[1:]:
+            self.send_buf = torch.empty((max(self.n_send, 1),) + tuple(U.shape[1:]),
+                                        dtype=U.dtype, device=U.device)
+        return self.send_buf
+
+    def send_slots(self) -> np.ndarray | None:
+        """Send-buffer row of every owned element (-1: not sent), or None
+        when some element goes to several peers (a slab one layer thick)."""
+        if self.n_send == 0 or len(np.unique(self.rows)) != len(self.rows):
+            return None
+        slot = np.full(self.part.n_owned, -1, dtype=np.int32)
+        slot[self.rows] = np.arange(self.n_send, dtype=np.int32)
+        return slot
+
+    def attach(self, op, stride: int) -> bool:
+        """Let ``op``'s last-touch passes fill the send buffer."""
+        import torch
+        from . import _native
+        slot = self.send_slots()
+        if slot is None:
+            return False
+        buf = self._buffer(torch.empty((0, stride), dtype=torch.float64, device=self.device))
+        _native.check(op._lib.mc_dg_set_send_rows(op._h, _native.ptr(slot), _native.ptr(buf),
+                                                  int(self.n_send)))
+        self.packed_by_kernel = True
+        return True
+
+    def stage_done(self, rk: bool) -> None:
+        """Called after a stage's color passes: with ``rk`` (an RK stage,
+        last touches updated U) the kernel-packed buffer is current."""
+        self.fresh = self.packed_by_kernel and rk
 
     def start(self, U):
-        """Gather the owned interface rows and post all sends / receives;
-        returns a handle for ``finish``.  With NCCL nothing blocks the host:
-        the transfers run on NCCL's stream, ordered after the gather."""
+        """Post all sends / receives; returns a handle for ``finish``.  With
+        NCCL nothing blocks the host: the transfers run on NCCL's stream,
+        ordered after the work already on the current stream."""
         import torch
         import torch.distributed as dist
-        ops, bufs = [], []
-        for q, ix in self.send_idx.items():
-            buf = U.index_select(0, ix).contiguous()
-            bufs.append(buf)
-            ops.append(dist.P2POp(dist.isend, buf, q))
-        recv = []
+        buf = self._buffer(U)
+        if not self.fresh and self.n_send:
+            torch.index_select(U, 0, self.send_idx, out=buf[: self.n_send])
+        self.fresh = False
+        ops = []
+        for q in self.peers:
+            a, b = self.offs[q]
+            ops.append(dist.P2POp(dist.isend, buf[a:b], q))
         for q, (a, b) in self.part.recv.items():
-            buf = torch.empty((b - a,) + tuple(U.shape[1:]), dtype=U.dtype, device=U.device)
-            recv.append((a, b, buf))
-            ops.append(dist.P2POp(dist.irecv, buf, q))
+            ops.append(dist.P2POp(dist.irecv, U[a:b], q))
         reqs = dist.batch_isend_irecv(ops) if ops else []
-        return reqs, recv, bufs
+        return reqs
 
     def finish(self, U, handle) -> None:
-        """Wait for the transfers (the current stream waits, not the host,
-        with NCCL) and write the ghost rows."""
-        reqs, recv, _bufs = handle
-        for req in reqs:
+        """Wait for the transfers (with NCCL the current stream waits, not
+        the host); the ghost rows are already in place."""
+        for req in handle:
             req.wait()
-        for a, b, buf in recv:
-            U[a:b] = buf
 
     def exchange(self, U) -> None:
         self.finish(U, self.start(U))

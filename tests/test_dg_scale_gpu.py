@@ -127,14 +127,14 @@ def pulse_error(n, p):
     ff = np.asarray(op.farfield, dtype=float)
     rho0, a = ff[0], ff[1:4] / ff[0]
     p0 = (op.gamma - 1) * (ff[-1] - 0.5 * rho0 * (a * a).sum())
-    c0 = np.array([0.35, 0.4, 0.45]) * n
-    R0 = 0.25 * n
-    T = 0.1 * n / np.linalg.norm(a)
+    c0 = np.full(3, 0.45 * n)
+    R0 = 0.4 * n
+    T = 0.05 * n / np.linalg.norm(a)
 
     def exact(t):
         def f(x):
             r = np.linalg.norm(x - c0 - a * t, axis=1) / R0
-            bump = np.where(r < 1, np.cos(0.5 * np.pi * np.minimum(r, 1)) ** 4, 0.0)
+            bump = np.where(r < 1, np.cos(0.5 * np.pi * np.minimum(r, 1)) ** 6, 0.0)
             rho = rho0 * (1 + 0.2 * bump)
             out = np.empty((len(x), 5))
             out[:, 0] = rho

@@ -191,3 +191,20 @@ def test_family_table_worked_example():
     assert fam.interior_edge_colors == (3, 2, 1)
     assert fam.children == (0, 1, 2, 3)
     assert len(ref.map.families) == 1 and ref.map.families == (fam,)
+
+
+def test_verify_coloring_diagnostics_match_reference():
+    """Defective colorings (repeated colors on an element, uncolored
+    surfaces, both) give the reference's exact Diagnostic list
+    (tests/golden/verify_cases.json, coloring.py:491-522)."""
+    import json
+    from conftest import GOLDEN, golden_mesh, load_golden
+    cases = json.loads((GOLDEN / "verify_cases.json").read_text())
+    assert len(cases) == 15
+    for case in cases:
+        m = golden_mesh(load_golden(case["mesh"]))
+        col = P.SurfaceColoring(np.asarray(case["colors"], dtype=np.int32), case["n_colors"])
+        got = [[d.code, d.message, d.element_id, d.surface_id]
+               for d in P.verify_coloring(m, col)]
+        assert got == case["diagnostics"], (case["mesh"], case["mode"])
+        assert got    # every case is defective

@@ -137,3 +137,48 @@ def test_two_rank_halo_exchange_reproduces_single_domain(tmp_path, kind):
         owned = np.load(tmp_path / f"o{r}.npy")
         Rl = np.load(tmp_path / f"r{r}.npy")
         assert np.array_equal(Rl, Rg[owned]), np.abs(Rl - Rg[owned]).max()
+
+
+def _worker_packed(rank, world, port, out):
+    """Three tet slabs: a gathered exchange, then an 'RK update' whose new
+    interface blocks are written into the send buffer through the send
+    slots (what the last-touch kernel does on the GPU), then an exchange
+    that posts the buffer as is."""
+    import torch
+    import torch.distributed as dist
+    from paper_1601_07613_b200.partition import HaloExchange
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m = P.gen_tet_prism(9, 2, 2)
+    c, _ = P.color(m)
+    lm, lc = P.apply_plan(m, c, P.build_plan(m, c))
+    owner = slab_owner(lm, world)
+    part = build_partition(lm, lc.colors, lc.n_colors, owner, rank)
+    Ug = np.arange(lm.n_elements * 4, dtype=np.float64).reshape(-1, 4)
+    U = torch.full((part.n_local, 4), np.nan, dtype=torch.float64)
+    U[: part.n_owned] = torch.from_numpy(Ug[part.owned])
+    halo = HaloExchange(part, "cpu")
+    halo.exchange(U)
+    ok1 = np.array_equal(U.numpy(), Ug[np.concatenate([part.owned, part.ghosts])])
+    slot = halo.send_slots()
+    assert slot is not None
+    U[: part.n_owned] += 1000.0                     # the stage's update of owned rows
+    buf = halo._buffer(U)
+    sel = slot >= 0
+    buf[torch.from_numpy(slot[sel]).long()] = U[: part.n_owned][torch.from_numpy(sel)]
+    halo.packed_by_kernel = True
+    halo.stage_done(rk=True)
+    assert halo.fresh
+    U[: part.n_owned] = torch.from_numpy(Ug[part.owned] + 1000.0)
+    halo.exchange(U)
+    ok2 = np.array_equal(U.numpy(), Ug[np.concatenate([part.owned, part.ghosts])] + 1000.0)
+    np.save(out + f"/ok{rank}.npy", np.array([ok1, ok2, not halo.fresh]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_three_rank_exchange_with_kernel_packed_send_rows(tmp_path):
+    world = 3
+    mp.spawn(_worker_packed, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert np.load(tmp_path / f"ok{r}.npy").all()
