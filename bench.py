@@ -97,7 +97,7 @@ def product_library_loaded() -> bool:
 
 
 # ------------------------------------------------------------- workloads
-def config_spec(name: str):
+def config_spec(name: str, device: str | None = "cuda"):
     """The product's build of a BASELINE config (GPU mesh assembly, native
     coloring, GPU AMR: bit-identical to the reference, see
     tests/test_config_golden_gpu.py)."""
@@ -105,7 +105,7 @@ def config_spec(name: str):
     if name not in CONFIGS:
         raise SystemExit(f"unknown config {name}")
     desc, physics, p, _ = CONFIGS[name]
-    dv = "cuda"
+    dv = device
     builds = {
         "c1": lambda: P.gen_tri_rect(64, 64),
         "c2": lambda: P.shuffle_elements(P.gen_tri_rect(708, 708, device=dv), 0, device=dv),

@@ -66,12 +66,14 @@ cudaError_t upload(T** dst, const T* src, int64_t count) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-int colored_grid(const mc_dg* h, int64_t n) {
+int colored_grid(const mc_dg* h, int64_t n, int variant) {
   // never launch more warps than surface tiles of the color
   const int64_t tiles = (n + h->ops->spw - 1) / h->ops->spw;
   const int64_t wpb = h->ops->threads / 32;
   const int64_t max_blocks = (tiles + wpb - 1) / wpb;
-  int grid = h->ops->grid_colored;
+  // MC_MIN_GRID=1: every variant at the smallest resident grid (round 1)
+  static const bool min_grid = std::getenv("MC_MIN_GRID") != nullptr;
+  int grid = min_grid ? h->ops->grid_colored : h->ops->grid_var[variant & 3];
   static const bool full = std::getenv("MC_FULL_GRID") != nullptr;   // A/B knob
   if (full || grid > max_blocks) grid = int(std::min<int64_t>(max_blocks, 1 << 30));
   if (h->grid_cap > 0 && grid > h->grid_cap) grid = h->grid_cap;
@@ -186,7 +188,8 @@ int colored_pass(mc_dg* h, double* U, double* R, const mcdg::RK* rk, cudaStream_
   for (int c = 1; c <= h->n_colors; ++c) {
     const int64_t b = h->bounds[c - 1], e = h->bounds[c];
     if (e == b) continue;
-    DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, colored_grid(h, e - b), s,
+    const int variant = ((rk && h->has_last[c]) ? 2 : 0) | (h->has_first[c] ? 1 : 0);
+    DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, colored_grid(h, e - b, variant), s,
                            h->has_first[c], h->has_last[c]));
   }
   return MC_OK;
@@ -251,7 +254,11 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   h->ng = d->n_ghosts;
   h->ns = d->n_surfaces;
   const int64_t w = int64_t(ops->neq) * ops->np;
-  h->stride = (w + 3) / 4 * 4;  // 32-byte aligned element blocks
+  // 32-byte aligned element blocks; MC_BLOCK_ALIGN=<doubles> (a multiple of
+  // 4) pads further, for DRAM-atom experiments (c4: 52 -> 56 doubles)
+  int64_t align = 4;
+  if (const char* a = std::getenv("MC_BLOCK_ALIGN")) align = std::max<int64_t>(4, std::atoi(a) / 4 * 4);
+  h->stride = (w + align - 1) / align * align;
   const int dim = ops->dim;
   std::vector<double> tables(ops->table_size);
   {
@@ -389,7 +396,8 @@ MC_API int mc_dg_color_range_pass(mc_dg* h, int color, int64_t begin, int64_t en
   if (begin < 0 || end < begin || c0 + end > c1) return mc_fail(MC_EINVAL, "bad surface range");
   const int64_t bb = c0 + begin, e = c0 + end;
   if (e == bb) return MC_OK;
-  const int grid = colored_grid(h, e - bb);
+  const int grid = colored_grid(h, e - bb, (rk_mode && h->has_last[color] ? 2 : 0) |
+                                               (h->has_first[color] ? 1 : 0));
   if (rk_mode == 0) {
     DG_TRY(h->ops->colored(h->view, U, R, nullptr, bb, e, grid, as_stream(stream),
                            h->has_first[color], h->has_last[color]));

@@ -326,6 +326,11 @@ struct Physics<ADV, DIM, NEQ> {
       Ft[r] = a * s[0];
     }
   }
+  // physical flux F[d][k] (the Jacobian is applied later, per element)
+  __device__ static __forceinline__ void pflux(const double* s, const Params& P, double* F) {
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) F[d] = P.vel[d] * s[0];
+  }
 };
 
 // fp64 reciprocal and square root for the flux: the hardware approximation
@@ -415,6 +420,19 @@ struct Physics<EULER, DIM, NEQ> {
                    0.5 * lam * (sR[1 + d] - sL[1 + d]);
     out[NEQ - 1] = 0.5 * ((sL[NEQ - 1] + pL) * vnL + (sR[NEQ - 1] + pR) * vnR) -
                    0.5 * lam * (sR[NEQ - 1] - sL[NEQ - 1]);
+  }
+
+  // physical flux F[d][k]: (m_d, m u_d + p e_d, (E + p) u_d)
+  __device__ static __forceinline__ void pflux(const double* s, const Params& P, double* F) {
+    double u[DIM], p, inv;
+    prim<true>(s, P, u, p, inv);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      F[d * NEQ + 0] = s[1 + d];
+#pragma unroll
+      for (int e = 0; e < DIM; ++e) F[d * NEQ + 1 + e] = s[1 + e] * u[d] + (e == d ? p : 0.0);
+      F[d * NEQ + NEQ - 1] = (s[NEQ - 1] + p) * u[d];
+    }
   }
 
   template <bool kFast = true>

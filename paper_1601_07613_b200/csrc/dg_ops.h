@@ -13,6 +13,9 @@ struct Ops {
   int threads;                                     // block size of the task kernels
   int spw;                                         // surfaces per warp
   int grid_colored, grid_volume, grid_uncolored;   // resident-grid sizes
+  // per colored-kernel variant, index (rk-update ? 2 : 0) | (volume ? 1 : 0):
+  // each variant has its own register budget, so its own resident grid
+  int grid_var[4];
   cudaError_t (*colored)(const View&, double* U, double* R, const RK* rk, int64_t b,
                          int64_t e, int grid, cudaStream_t s, bool has_first, bool has_last);
   cudaError_t (*volume)(const View&, const double* U, double* R, int grid, cudaStream_t s);
@@ -108,14 +111,13 @@ struct Instance {
     cudaError_t err;
     int g2 = 0;
     if constexpr (T::OK) {
-      if ((err = fit((const void*)k_tpe_colored<C, PH, true, true>, T::SMEM, T::THREADS, &o->grid_colored))) return err;
-      if ((err = fit((const void*)k_tpe_colored<C, PH, false, true>, T::SMEM, T::THREADS, &g2))) return err;
-      if (g2 < o->grid_colored) o->grid_colored = g2;
-      for (const void* fn : {(const void*)k_tpe_colored<C, PH, true, false>,
-                             (const void*)k_tpe_colored<C, PH, false, false>}) {
-        if ((err = fit(fn, T::SMEM_SURF, T::THREADS, &g2))) return err;
-        if (g2 < o->grid_colored) o->grid_colored = g2;
-      }
+      if ((err = fit((const void*)k_tpe_colored<C, PH, true, true>, T::SMEM, T::THREADS, &o->grid_var[3]))) return err;
+      if ((err = fit((const void*)k_tpe_colored<C, PH, false, true>, T::SMEM, T::THREADS, &o->grid_var[1]))) return err;
+      if ((err = fit((const void*)k_tpe_colored<C, PH, true, false>, T::SMEM_SURF, T::THREADS, &o->grid_var[2]))) return err;
+      if ((err = fit((const void*)k_tpe_colored<C, PH, false, false>, T::SMEM_SURF, T::THREADS, &o->grid_var[0]))) return err;
+      o->grid_colored = o->grid_var[0];
+      for (int k = 1; k < 4; ++k)
+        if (o->grid_var[k] < o->grid_colored) o->grid_colored = o->grid_var[k];
       if ((err = fit((const void*)k_tpe_volume<C, PH>, T::SMEM, T::THREADS, &o->grid_volume))) return err;
       if ((err = fit((const void*)k_tpe_uncolored<C, PH, true>, T::SMEM, T::THREADS, &o->grid_uncolored))) return err;
       if ((err = fit((const void*)k_tpe_uncolored<C, PH, false>, T::SMEM, T::THREADS, &g2))) return err;
@@ -123,6 +125,8 @@ struct Instance {
     } else {
       if ((err = fit((const void*)k_surface_colored<C, PH, true>, C::SMEM, C::THREADS, &o->grid_colored))) return err;
       if ((err = fit((const void*)k_surface_colored<C, PH, false>, C::SMEM, C::THREADS, &g2))) return err;
+      o->grid_var[2] = o->grid_var[3] = o->grid_colored;
+      o->grid_var[0] = o->grid_var[1] = g2;
       if (g2 < o->grid_colored) o->grid_colored = g2;
       if ((err = fit((const void*)k_volume<C, PH>, C::VSMEM, C::THREADS, &o->grid_volume))) return err;
       if ((err = fit((const void*)k_surface_uncolored<C, PH, true>, C::SMEM, C::THREADS, &o->grid_uncolored))) return err;
@@ -148,7 +152,7 @@ struct Instance {
   static Ops* ops() {
     static Ops o{C::DIM, C::NEQ, C::NP, C::NQF, C::NQV, C::NCODES, C::T_SIZE,
                  T::OK ? T::THREADS : C::THREADS, T::OK ? T::SW : C::SPW,
-                 0, 0, 0, &colored, &volume, &uncolored, &gather, &init, C::S_TOTAL,
+                 0, 0, 0, {0, 0, 0, 0}, &colored, &volume, &uncolored, &gather, &init, C::S_TOTAL,
                  &stage_global, &upload_const, C::NPL, C::P1PROJ ? 1 : 0};
     return &o;
   }

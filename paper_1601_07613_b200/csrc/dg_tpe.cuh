@@ -183,24 +183,29 @@ constexpr int grad_shell(int j) {
   return simplex_modes<K>(d - 1);
 }
 
-// Volume integral through P_{p-1} (Cfg::P1PROJ, simplices): the contravariant
+// Volume integral through P_{p-1} (Cfg::P1PROJ, simplices): the physical
 // fluxes are first projected onto the NPL modes of P_{p-1} with the weights
-// folded in (Pm[r][k][m] = sum_q w_q phi_m(q) Ft_r(q)[k]), then lifted once
-// per element, acc[k][j] += sum_r sum_m D_r[j][m] Pm[r][k][m] with D's
-// zero blocks skipped at compile time (c4: 3 x 4 instead of 3 x 10
-// multiply-adds per point and equation).  Two lanes per side additionally
-// split the volume points: at each point pair, lane h evaluates the flux of
-// point 2i+h only (the traces and the fluxes of the other lane's equations
-// cross by shuffles), so every flux is evaluated once, not twice.
+// folded in (Pd[d][k][m] = sum_q w_q phi_m(q) F_d(q)[k]), the element's
+// (constant) inverse Jacobian turns them into contravariant moments once,
+// Pm[r] = sum_d Jinv[r][d] Pd[d], and they are lifted once per element,
+// acc[k][j] += sum_r sum_m D_r[j][m] Pm[r][k][m], with D's zero blocks
+// skipped at compile time (c4: 3 x 4 instead of 3 x 10 multiply-adds per
+// point and equation, no Jacobian per point).  Two lanes per side also
+// split the volume points: at each point pair, lane h evaluates the flux
+// of point 2i+h only (the traces and the fluxes of the other lane's
+// equations cross by shuffles), so every flux is evaluated once, not twice.
 template <class C, int PH>
 __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (&u)[Tpe<C>::WH],
-                                              const double (&ji)[C::DIM * C::DIM], int h,
+                                              const double* __restrict__ jinv_e, int h,
                                               int nown, bool mine, const Params& P,
                                               double (&acc)[Tpe<C>::WH]) {
   constexpr int NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH, DIM = C::DIM, M = C::NPL;
   constexpr int H = Tpe<C>::H, WH = Tpe<C>::WH;
   const double* wpsi = vphi + (C::S_WPSI - C::S_VPHI);
   const double* dmat = vphi + (C::S_DMAT - C::S_VPHI);
+  // the Jacobian is needed only at the end: pull its line into L1 now
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(jinv_e));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(jinv_e + DIM * DIM - 1));
   double Pm[DIM][NEQH][M];
 #pragma unroll
   for (int r = 0; r < DIM; ++r)
@@ -214,15 +219,15 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (
 #pragma unroll
     for (int k = 0; k < NEQH; ++k) own[k] = tdot<NP, WH>(vphi + q * C::NPP, u, k * NP);
     assemble_state<C>(own, h, s);
-    double Ft[DIM * NEQ];
-    Physics<PH, DIM, NEQ>::vflux(s, ji, P, Ft);
+    double F[DIM * NEQ];
+    Physics<PH, DIM, NEQ>::pflux(s, P, F);
 #pragma unroll
-    for (int r = 0; r < DIM; ++r)
+    for (int d = 0; d < DIM; ++d)
 #pragma unroll
       for (int k = 0; k < NEQH; ++k) {
-        const double f = (mine && k < nown) ? own_part<C>(Ft + r * NEQ, h, k) : 0.0;
+        const double f = (mine && k < nown) ? own_part<C>(F + d * NEQ, h, k) : 0.0;
 #pragma unroll
-        for (int m = 0; m < M; ++m) Pm[r][k][m] = fma(wpsi[q * M + m], f, Pm[r][k][m]);
+        for (int m = 0; m < M; ++m) Pm[d][k][m] = fma(wpsi[q * M + m], f, Pm[d][k][m]);
       }
   };
   if constexpr (H == 1) {
@@ -241,27 +246,46 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (
         ot[k] = __shfl_xor_sync(kFull, h ? a : b, 1);    // partner's traces at my point
         mt[k] = h ? b : a;                                // mine at my point (q0 + h)
       }
-      double s[NEQ], Ft[DIM * NEQ];
+      double s[NEQ], F[DIM * NEQ];
 #pragma unroll
       for (int e = 0; e < NEQ; ++e)
         s[e] = (e < NA) ? (h == 0 ? mt[e] : ot[e]) : (h == 1 ? mt[e - NA] : ot[e - NA]);
-      Physics<PH, DIM, NEQ>::vflux(s, ji, P, Ft);
+      Physics<PH, DIM, NEQ>::pflux(s, P, F);
 #pragma unroll
-      for (int r = 0; r < DIM; ++r)
+      for (int d = 0; d < DIM; ++d)
 #pragma unroll
         for (int k = 0; k < NEQH; ++k) {
-          const double fm = own_part<C>(Ft + r * NEQ, h, k);        // my eq, my point
-          const double fr = __shfl_xor_sync(kFull, own_part<C>(Ft + r * NEQ, h ^ 1, k), 1);
+          const double fm = own_part<C>(F + d * NEQ, h, k);         // my eq, my point
+          const double fr = __shfl_xor_sync(kFull, own_part<C>(F + d * NEQ, h ^ 1, k), 1);
           const bool on = mine && k < nown;
           const double f0 = on ? (h ? fr : fm) : 0.0;              // at q0
           const double f1 = on ? (h ? fm : fr) : 0.0;              // at q1
 #pragma unroll
           for (int m = 0; m < M; ++m)
-            Pm[r][k][m] = fma(wpsi[q1 * M + m], f1, fma(wpsi[q0 * M + m], f0, Pm[r][k][m]));
+            Pm[d][k][m] = fma(wpsi[q1 * M + m], f1, fma(wpsi[q0 * M + m], f0, Pm[d][k][m]));
         }
     }
     if constexpr (C::NQV % 2) point(C::NQV - 1);
   }
+  // physical -> contravariant moments with the element's inverse Jacobian
+  double ji[DIM * DIM];
+#pragma unroll
+  for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
+#pragma unroll
+  for (int k = 0; k < NEQH; ++k)
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double pd[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) pd[d] = Pm[d][k][m];
+#pragma unroll
+      for (int r = 0; r < DIM; ++r) {
+        double t = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) t = fma(ji[r * DIM + d], pd[d], t);
+        Pm[r][k][m] = t;
+      }
+    }
 #pragma unroll
   for (int k = 0; k < NEQH; ++k)
 #pragma unroll
@@ -286,6 +310,12 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   const double* vphi = vol_tables<C, true>(st);
   const double* vdphi = vphi + (C::S_VDPHI - C::S_VPHI);
   const double* vw = vphi + (C::S_VW - C::S_VPHI);
+  // two lanes per side (tets): c4 first-touch color 4.91 -> 4.57 ms; one
+  // lane (c2 triangles) measured slower (color 1 3.55 -> 3.27 TB/s)
+  if constexpr (C::P1PROJ && (Tpe<C>::H == 2 || kP1ProjH1)) {
+    tpe_volume_p1<C, PH>(vphi, u, jinv_e, h, nown, mine, P, acc);
+    return;
+  }
   double ji[DIM * DIM];
 #pragma unroll
   for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
@@ -353,12 +383,6 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
     return;
   }
 #endif
-  // two lanes per side (tets): c4 first-touch color 4.91 -> 4.57 ms; one
-  // lane (c2 triangles) measured slower (color 1 3.55 -> 3.27 TB/s)
-  if constexpr (C::P1PROJ && (Tpe<C>::H == 2 || kP1ProjH1)) {
-    tpe_volume_p1<C, PH>(vphi, u, ji, h, nown, mine, P, acc);
-    return;
-  }
   constexpr int kUnroll = kVolUnroll<Tpe<C>::H>;
 #pragma unroll kUnroll
   for (int q = 0; q < C::NQV; ++q) {
@@ -826,6 +850,9 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 #ifndef MC_TPE_MINB_VOL
 #define MC_TPE_MINB_VOL 0   // 0: Tpe<C>::MINB
 #endif
+#ifndef MC_TPE_MINB_VOL2
+#define MC_TPE_MINB_VOL2 2  // two lanes per side, first-touch passes
+#endif
 
 struct TpeLane {
   int lane, side, h, grp, nown, eq0;
@@ -851,7 +878,7 @@ template <class C, int PH, bool kRK, bool kVol>
 __global__ void __launch_bounds__(Tpe<C>::THREADS,
                                   Tpe<C>::H == 2
                                       ? ((!kVol && !kRK) ? MC_TASKS_MINB_SURF
-                                                                           : Tpe<C>::MINB)
+                                         : kVol ? MC_TPE_MINB_VOL2 : Tpe<C>::MINB)
                                   : kVol ? (MC_TPE_MINB_VOL ? MC_TPE_MINB_VOL : Tpe<C>::MINB)
                                   : (kRK ? MC_TPE_MINB_RK : MC_TPE_MINB_SURF))
 k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
@@ -895,10 +922,13 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
     }
-    if (t.owner && !first) tload_rw<WH, kWhole, T::V4>(R + off, n, acc);
-    else {
+    // first-touch passes: the volume integral first, then the residual
+    // blocks of the sides touched before (acc is not live during the volume)
+    if (kVol || !(t.owner && !first)) {
 #pragma unroll
       for (int j = 0; j < WH; ++j) acc[j] = 0.0;
+    } else {
+      tload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     }
     if constexpr (kVol) {
       const double* jp = v.jinv + int64_t(first ? t.e : 0) * (C::DIM * C::DIM);
@@ -907,6 +937,7 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
       } else if (__any_sync(kFull, first)) {   // the whole warp takes part in the shuffles
         tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc);
       }
+      if (t.owner && !first) tload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     }
     tpe_surface<C, PH, (kVol ? T::TASKS : T::TASKS_SURF)>(st, t, ln.side, ln.h, ln.nown, u, v.prm,
                                                           acc, ln.grp, ws);

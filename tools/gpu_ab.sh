@@ -3,7 +3,7 @@
 #   edit the loop at the bottom, then: gpurun -- 'bash tools/gpu_ab.sh'
 run() {  # $1 = defines, $2 = env assignment
   MC_DEFINES="$1" python paper_1601_07613_b200/_build.py --force > /dev/null
-  env $2 python bench.py --no-cpu --e2e-steps 1 ${BENCH_ARGS} > gpurun_out/ab.json 2>&1
+  env $2 python bench.py --no-cpu --no-variants --e2e-steps 1 ${BENCH_ARGS} > gpurun_out/ab.json 2>&1
   python -c "import json,sys; d=json.load(open('gpurun_out/ab.json')); print('[$1 | $2 | ${BENCH_ARGS}]', round(d['value']/1e9,3), 'G edges/s', round(d['ms_per_step'],3), 'ms', round(d['roofline']['frac'],3), {k: round(v) for k,v in d['roofline']['per_color_gbs'].items()})" >> gpurun_out/ab_summary.txt 2>&1 || tail -3 gpurun_out/ab.json >> gpurun_out/ab_summary.txt
 }
 rm -f gpurun_out/ab_summary.txt

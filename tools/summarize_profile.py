@@ -74,7 +74,7 @@ import bench  # noqa: E402
 import paper_1601_07613_b200 as P  # noqa: E402
 from paper_1601_07613_b200.dg.layout import build_surface_list  # noqa: E402
 from paper_1601_07613_b200.dg.basis import reference_tables  # noqa: E402
-spec = bench.config_spec(cfg)
+spec = bench.config_spec(cfg, device=None)
 obj = spec["build"]()
 if isinstance(obj, tuple):
     mesh, col = obj[0].mesh, obj[1]

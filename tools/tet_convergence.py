@@ -47,10 +47,12 @@ def err(n, p, physics, cfl, travel, power=6):
 if __name__ == "__main__":
     cfl = float(sys.argv[1]) if len(sys.argv) > 1 else 0.1
     travel = float(sys.argv[2]) if len(sys.argv) > 2 else 0.05
+    ns = tuple(int(x) for x in sys.argv[3].split(",")) if len(sys.argv) > 3 else (8, 16, 32)
+    degrees = tuple(int(x) for x in sys.argv[4].split(",")) if len(sys.argv) > 4 else (1, 2, 3)
     for physics in ("advection", "euler"):
-        for p in (1, 2, 3):
-            es = [err(n, p, physics, cfl, travel) for n in (8, 16, 32)]
-            rates = [np.log2(es[i][0] / es[i + 1][0]) for i in range(2)]
+        for p in degrees:
+            es = [err(n, p, physics, cfl, travel) for n in ns]
+            rates = [np.log2(es[i][0] / es[i + 1][0]) for i in range(len(ns) - 1)]
             print(f"{physics} p={p} cfl={cfl} travel={travel}: errors "
                   f"{[f'{e:.3e}' for e, _ in es]} steps {[s for _, s in es]} rates "
                   f"{[round(r, 2) for r in rates]}", flush=True)
