@@ -110,6 +110,22 @@ __device__ __forceinline__ double tdot(const double* row, const double (&u)[N], 
   return t;
 }
 
+// As tdot with two partial sums (even / odd j): half the dependent-FMA
+// chain, for latency-bound trace loops
+template <int NP, int N>
+__device__ __forceinline__ double tdot2(const double* row, const double (&u)[N], int off) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+  double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < NP / 2; ++j) {
+    const double2 a = r2[j];
+    t0 = fma(a.x, u[off + 2 * j], t0);
+    t1 = fma(a.y, u[off + 2 * j + 1], t1);
+  }
+  if constexpr (NP % 2) t0 = fma(row[NP - 1], u[off + NP - 1], t0);
+  return t0 + t1;
+}
+
 template <int NP, int N>
 __device__ __forceinline__ void taxpy(const double* row, double f, double (&acc)[N], int off) {
   const double2* r2 = reinterpret_cast<const double2*>(row);
@@ -251,19 +267,43 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (
       for (int e = 0; e < NEQ; ++e)
         s[e] = (e < NA) ? (h == 0 ? mt[e] : ot[e]) : (h == 1 ? mt[e - NA] : ot[e - NA]);
       Physics<PH, DIM, NEQ>::pflux(s, P, F);
+      // weights of my point and of the partner's (selected once per pair,
+      // not per flux component).  Lanes whose element takes no volume
+      // term here (not first touch, no element) accumulate garbage that
+      // never leaves the lane pair and is never stored: the caller
+      // replaces their acc (residual load) or does not store it.
+#ifdef MC_PAIR_WSEL   // weights selected once per pair: more registers, c4 -10 %
+      double wm[M], wo[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const double w0 = wpsi[q0 * M + m], w1 = wpsi[q1 * M + m];
+        wm[m] = h ? w1 : w0;
+        wo[m] = h ? w0 : w1;
+      }
 #pragma unroll
       for (int d = 0; d < DIM; ++d)
 #pragma unroll
         for (int k = 0; k < NEQH; ++k) {
           const double fm = own_part<C>(F + d * NEQ, h, k);         // my eq, my point
           const double fr = __shfl_xor_sync(kFull, own_part<C>(F + d * NEQ, h ^ 1, k), 1);
+#pragma unroll
+          for (int m = 0; m < M; ++m) Pm[d][k][m] = fma(wo[m], fr, fma(wm[m], fm, Pm[d][k][m]));
+        }
+#else   // per-component selects of the two points' fluxes (measured faster)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d)
+#pragma unroll
+        for (int k = 0; k < NEQH; ++k) {
+          const double fm = own_part<C>(F + d * NEQ, h, k);
+          const double fr = __shfl_xor_sync(kFull, own_part<C>(F + d * NEQ, h ^ 1, k), 1);
           const bool on = mine && k < nown;
-          const double f0 = on ? (h ? fr : fm) : 0.0;              // at q0
-          const double f1 = on ? (h ? fm : fr) : 0.0;              // at q1
+          const double f0 = on ? (h ? fr : fm) : 0.0;
+          const double f1 = on ? (h ? fm : fr) : 0.0;
 #pragma unroll
           for (int m = 0; m < M; ++m)
             Pm[d][k][m] = fma(wpsi[q1 * M + m], f1, fma(wpsi[q0 * M + m], f0, Pm[d][k][m]));
         }
+#endif
     }
     if constexpr (C::NQV % 2) point(C::NQV - 1);
   }
@@ -577,13 +617,22 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
 #pragma unroll
       for (int k = 0; k < NEQH; ++k) {
         if (k < nown) {
-          const double v = t.has ? tdot<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP)
-                                 : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
+          // MC_TRACE_ILP: two half-length FMA chains (c4 surface colors -6 %
+          // at the 168-register budget of 3 blocks per SM)
+#ifndef MC_TRACE_ILP
+          const double tv = tdot<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP);
+#else
+          const double tv = tdot2<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP);
+#endif
+          const double v = t.has ? tv : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
           tr[((g * SW + grp) * 2 + side) * SV + eq0 + k] = v;
         }
       }
     }
     __syncwarp();
+#ifdef MC_TASK_UNROLL   // interleaved task pairs: c4 surface colors -4 %
+#pragma unroll 2
+#endif
     for (int q = lane; q < SW * C::NQF; q += 32) {
       const int g = q / SW, gs = q - g * SW;
       const int f = flg[gs];
@@ -844,14 +893,20 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 #ifndef MC_TPE_MINB_RK
 #define MC_TPE_MINB_RK 3
 #endif
+// two lanes per side: blocks per SM of the surface-only (3: c4 colors 2-3
+// 3.98 -> 4.40 TB/s, c3 +1 %), first-touch (tets 3: +5 %; quads keep 2:
+// -18 %) and last-touch passes; each variant gets its own resident grid
 #ifndef MC_TASKS_MINB_SURF
-#define MC_TASKS_MINB_SURF 2
+#define MC_TASKS_MINB_SURF 3
+#endif
+#ifndef MC_TPE_MINB_RK2
+#define MC_TPE_MINB_RK2 2
 #endif
 #ifndef MC_TPE_MINB_VOL
 #define MC_TPE_MINB_VOL 0   // 0: Tpe<C>::MINB
 #endif
 #ifndef MC_TPE_MINB_VOL2
-#define MC_TPE_MINB_VOL2 2  // two lanes per side, first-touch passes
+#define MC_TPE_MINB_VOL2 3  // two lanes per side, first-touch passes (tets)
 #endif
 
 struct TpeLane {
@@ -878,7 +933,8 @@ template <class C, int PH, bool kRK, bool kVol>
 __global__ void __launch_bounds__(Tpe<C>::THREADS,
                                   Tpe<C>::H == 2
                                       ? ((!kVol && !kRK) ? MC_TASKS_MINB_SURF
-                                         : kVol ? MC_TPE_MINB_VOL2 : Tpe<C>::MINB)
+                                         : kVol ? (C::DIM == 3 ? MC_TPE_MINB_VOL2 : 2)
+                                                : MC_TPE_MINB_RK2)
                                   : kVol ? (MC_TPE_MINB_VOL ? MC_TPE_MINB_VOL : Tpe<C>::MINB)
                                   : (kRK ? MC_TPE_MINB_RK : MC_TPE_MINB_SURF))
 k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
