@@ -510,7 +510,7 @@ __device__ __forceinline__ TpeSide tpe_side(const View& v, int64_t s, int64_t en
 // on the index load and then the block load).
 template <class C>
 __device__ __forceinline__ TpeSide tpe_side_pre(const View& v, int64_t s, int64_t end, int side,
-                                                int e_pre) {
+                                                int e_pre, const uint32_t* code_pre = nullptr) {
   TpeSide t;
   t.valid = s < end;
   t.code = 0;
@@ -519,7 +519,7 @@ __device__ __forceinline__ TpeSide tpe_side_pre(const View& v, int64_t s, int64_
   t.n[1] = 0.0;
   t.n[2] = 0.0;
   if (t.valid) {
-    t.code = __ldg(v.code + s);
+    t.code = code_pre ? *code_pre : __ldg(v.code + s);
     const double* gm = v.geom + s * C::GEOM;
 #pragma unroll
     for (int d = 0; d < C::DIM; ++d) t.n[d] = __ldg(gm + d);
@@ -620,11 +620,12 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
           // MC_TRACE_ILP: two half-length FMA chains (c4 surface colors -6 %
           // at the 168-register budget of 3 blocks per SM)
 #ifndef MC_TRACE_ILP
-          const double tv = tdot<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP);
+          const double v = t.has ? tdot<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP)
+                                 : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
 #else
-          const double tv = tdot2<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP);
+          const double v = t.has ? tdot2<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP)
+                                 : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
 #endif
-          const double v = t.has ? tv : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
           tr[((g * SW + grp) * 2 + side) * SV + eq0 + k] = v;
         }
       }
@@ -953,18 +954,31 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
 #ifndef MC_NO_E_PREFETCH
   const int32_t* eidx = ln.side ? v.right : v.left;
   int e_next = -1;
+#ifdef MC_CODE_PREFETCH
+  uint32_t c_next = 0;   // the surface code word one tile ahead as well
+#endif
   {
     const int64_t s0 = begin + warp * T::SW + ln.grp;
     if (s0 < end) e_next = __ldg(eidx + s0);
+#ifdef MC_CODE_PREFETCH
+    if (s0 < end) c_next = __ldg(v.code + s0);
+#endif
   }
 #endif
   for (int64_t tile = begin + warp * T::SW; tile < end; tile += nwarp * T::SW) {
     const int64_t s = tile + ln.grp;
 #ifndef MC_NO_E_PREFETCH
+#ifdef MC_CODE_PREFETCH
+    const TpeSide t = tpe_side_pre<C>(v, s, end, ln.side, e_next, &c_next);
+#else
     const TpeSide t = tpe_side_pre<C>(v, s, end, ln.side, e_next);
+#endif
     {
       const int64_t sn = s + nwarp * T::SW;
       e_next = sn < end ? __ldg(eidx + sn) : -1;
+#ifdef MC_CODE_PREFETCH
+      c_next = sn < end ? __ldg(v.code + sn) : 0u;
+#endif
     }
 #else
     const TpeSide t = tpe_side<C>(v, s, end, ln.side);
@@ -999,6 +1013,11 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
                                                           acc, ln.grp, ws);
     if (t.owner) {
       if (last) {
+#ifdef MC_RK_RELOAD_U
+        // re-read the element's own block (L2) instead of keeping u live
+        // through the surface work (fewer registers in the last-touch pass)
+        if constexpr (kRK && !kVol) tload<WH, kWhole, T::V4>(U + off, n, u);
+#endif
         if (rk.save_u0) tstore<WH, kWhole, T::V4>(rk.U0 + off, n, u);
         if (rk.a != 0.0) {
           double u0[WH];

@@ -504,10 +504,10 @@ class DGOperator:
             J = np.stack([X[:, 1] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)
         else:
             J = np.stack([X[:, r + 1] - X[:, 0] for r in range(self.dim)], axis=2)
-        out = np.empty((self.n_elements, self.n_equations, self.n_basis))
+        out = np.empty((self.mesh.n_elements, self.n_equations, self.n_basis))
         chunk = 1 << 16
-        for a in range(0, self.n_elements, chunk):
-            b = min(a + chunk, self.n_elements)
+        for a in range(0, self.mesh.n_elements, chunk):
+            b = min(a + chunk, self.mesh.n_elements)
             x = X[a:b, 0][:, None, :] + np.einsum("erk,qk->eqr", J[a:b], pts)
             vals = fn(x.reshape(-1, self.dim)).reshape(b - a, len(w), self.n_equations)
             out[a:b] = np.einsum("q,qj,eqk->ekj", w, phi, vals)
