@@ -83,11 +83,16 @@ def test_send_buffer_packing_stays_inside(cuda):
     big, buf = guarded(h.n_send, op.stride)
     _native.check(op._lib.mc_dg_set_send_rows(op._h, _native.ptr(slot), _native.ptr(buf),
                                               int(h.n_send)))
-    U = torch.from_numpy(op.to_internal(op.initial_state("wave"))).cuda()
+    Uu = op.initial_state("wave")
+    Ui = op.to_internal(Uu)
+    inv = np.argsort(op.plan.element_perm)              # layout id -> user id
+    Ui[op.n_elements:, : op.block_width()] = Uu[inv[op.part.ghosts]].reshape(len(op.part.ghosts), -1)
+    U = torch.from_numpy(Ui).cuda()
     w = op.work_device()
     for c in range(1, op.n_colors + 1):
         op.color_pass_device(c, U, w[0], w[1], 2, 0.0, 1.0, 1e-3)
     torch.cuda.synchronize()
     assert guards_intact(big, h.n_send)
     rows = torch.as_tensor(h.rows, device="cuda")
+    assert torch.isfinite(U).all()
     assert torch.equal(buf[: h.n_send], U.index_select(0, rows))
