@@ -195,7 +195,7 @@ def launch_bytes(op, color: int, rk_mode: int, a: float) -> int:
     b0, b1 = sl.bounds[color - 1], sl.bounds[color]
     code = sl.code[b0:b1].astype(np.int64)
     right = sl.right[b0:b1]
-    D = op.n_equations * op.n_basis * 8
+    D = op.n_equations * op.n_basis * (4 if getattr(op, "state", "f64") == "f32" else 8)
     dim = op.dim
     meta = 4 + 4 + 4 + 8 * (dim + 2)
     total = meta * (b1 - b0)
@@ -368,6 +368,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--layouts", action="store_true",
                     help="time the paper's Table 7 layouts on c2 instead")
+    ap.add_argument("--state", default="f64", choices=["f64", "f32"],
+                    help="element-block storage (f32: half the bytes, fp64 arithmetic, the north "
+                         "star's 1e-5 tolerance; not the headline)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -387,7 +390,7 @@ def main():
 
     spec = config_spec(args.config)
     t_setup = time.perf_counter()
-    op = build_operator(spec, world=world, rank=rank)
+    op = build_operator(spec, world=world, rank=rank, state=args.state)
     t_setup = time.perf_counter() - t_setup
     U_host = op.initial_state("wave")
     dt = op.stable_dt(0.2)
@@ -396,7 +399,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         dt = float(t.item())
         dist.barrier()
-    U = torch.from_numpy(op.to_internal(U_host)).cuda()
+    U = op.to_device(U_host)
     work = op.work_device()
     U0, R = work[0], work[1]
     stream = torch.cuda.current_stream()
@@ -513,7 +516,7 @@ def main():
     e2e_value = 3 * ns_global / e2e_s
 
     comparisons = None
-    if not args.no_variants and world == 1:
+    if not args.no_variants and world == 1 and args.state == "f64":
         comparisons = variants(op, U_host, stream)
 
     cpu = None
@@ -529,7 +532,8 @@ def main():
         "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (density wave on far-field stream)",
+        "dtype": "f64" if args.state == "f64" else "f32 storage, f64 arithmetic",
+        "data": "synthetic (density wave on far-field stream)",
         "config": {"workload": spec["desc"] + ("" if world == 1 else
                                                f", split over {world} GPUs"),
                    "elements": ne_global, "surfaces": ns_global, "colors": nc,
@@ -540,7 +544,8 @@ def main():
                              "color-1 pairs in Z-order)" if op.ordering == "sfc"
                              else op.ordering,
                    "kernel": kernel_name(op),
-                   "l2": f"inputs larger than L2 (state {op.n_local * op.stride * 8 / 1e9:.2f}"
+                   "l2": f"inputs larger than L2 (state "
+                         f"{op.n_local * op.stride * (4 if args.state == 'f32' else 8) / 1e9:.2f}"
                          " GB x 3 arrays, no flush needed)",
                    "parallelism": "single-GPU" if world == 1 else
                    f"domain decomposition x{world} (slabs, NCCL ghost exchange per stage)",

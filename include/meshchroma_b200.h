@@ -189,6 +189,11 @@ typedef struct mc_dg_desc {
   double gamma;
   double velocity[3];
   double farfield[5];
+  /* state storage: 0 = fp64 element blocks; 1 = fp32 blocks (all arithmetic
+   * stays fp64; colored strategy and steppers only; the north star's
+   * 1e-5 tolerance).  Every U / U0 / R / work / send-buffer pointer of an
+   * fp32 operator points to floats, strides count floats. */
+  int state_f32;
 } mc_dg_desc;
 
 typedef struct mc_dg mc_dg;

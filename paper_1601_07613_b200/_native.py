@@ -61,6 +61,7 @@ class DGDesc(C.Structure):
         ("vol_w", C.c_void_p),
         ("gamma", C.c_double), ("velocity", C.c_double * 3),
         ("farfield", C.c_double * 5),
+        ("state_f32", C.c_int),
     ]
 
 

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "dg_ops.h"
@@ -27,7 +28,9 @@ struct mc_dg {
   double *d_geom = nullptr, *d_jinv = nullptr, *d_tables = nullptr, *d_ptables = nullptr;
   int64_t* d_slot_ptr = nullptr;
   double* d_buffer = nullptr;      // 2*ns blocks (buffered strategy)
-  double* d_host_U = nullptr;      // host path scratch: U, U0, R
+  char* d_host_U = nullptr;        // host path scratch: U, U0, R (state type)
+  int f32 = 0;                     // fp32 state storage (element blocks of floats)
+  int64_t esize = 8;               // bytes per state value
   cudaStream_t stream = nullptr;
   // one SSP-RK3 step captured as a CUDA graph (9-12 launches replayed with
   // one cudaGraphLaunch), keyed by the arguments baked into it
@@ -66,6 +69,13 @@ cudaError_t upload(T** dst, const T* src, int64_t count) {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// `blocks` element blocks past `base` in the operator's state type
+template <class P>
+P* at_blocks(P* base, const mc_dg* h, int64_t blocks) {
+  using B = typename std::conditional<std::is_const<P>::value, const char, char>::type;
+  return reinterpret_cast<P*>(reinterpret_cast<B*>(base) + blocks * h->stride * h->esize);
+}
+
 int colored_grid(const mc_dg* h, int64_t n, int variant) {
   // never launch more warps than surface tiles of the color
   const int64_t tiles = (n + h->ops->spw - 1) / h->ops->spw;
@@ -88,25 +98,27 @@ int capped(const mc_dg* h, int grid) {
 // order) <-> internal layout (renumbered rows, `stride`-padded blocks); one
 // thread per internal double, coalesced on the internal side, W contiguous
 // doubles per row on the user side
+template <class S>
 __global__ void k_user_to_internal(const double* __restrict__ user, const int64_t* __restrict__ src,
-                                   double* __restrict__ U, int64_t rows, int W, int stride) {
+                                   S* __restrict__ U, int64_t rows, int W, int stride) {
   const int64_t total = rows * stride;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = i / stride;
     const int j = int(i - r * stride);
-    U[i] = j < W ? __ldg(user + __ldg(src + r) * W + j) : 0.0;
+    U[i] = S(j < W ? __ldg(user + __ldg(src + r) * W + j) : 0.0);
   }
 }
 
-__global__ void k_internal_to_user(const double* __restrict__ U, const int64_t* __restrict__ src,
+template <class S>
+__global__ void k_internal_to_user(const S* __restrict__ U, const int64_t* __restrict__ src,
                                    double* __restrict__ user, int64_t rows, int W, int stride) {
   const int64_t total = rows * W;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = i / W;
     const int j = int(i - r * W);
-    user[__ldg(src + r) * W + j] = U[r * stride + j];
+    user[__ldg(src + r) * W + j] = double(U[r * stride + j]);
   }
 }
 
@@ -184,13 +196,13 @@ int p1_tables(const Ops* ops, const mc_dg_desc* d, double* out) {
   return MC_OK;
 }
 
-int colored_pass(mc_dg* h, double* U, double* R, const mcdg::RK* rk, cudaStream_t s) {
+int colored_pass(mc_dg* h, void* U, void* R, const mcdg::RK* rk, cudaStream_t s) {
   for (int c = 1; c <= h->n_colors; ++c) {
     const int64_t b = h->bounds[c - 1], e = h->bounds[c];
     if (e == b) continue;
     const int variant = ((rk && h->has_last[c]) ? 2 : 0) | (h->has_first[c] ? 1 : 0);
     DG_TRY(h->ops->colored(h->view, U, R, rk, b, e, colored_grid(h, e - b, variant), s,
-                           h->has_first[c], h->has_last[c]));
+                           h->has_first[c], h->has_last[c], h->f32));
   }
   return MC_OK;
 }
@@ -214,6 +226,8 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   if (d->n_face_codes != ops->ncodes || d->n_face_q != ops->nqf || d->n_vol_q != ops->nqv ||
       d->n_basis != ops->np)
     return mc_fail(MC_EINVAL, "reference tables do not match the compiled kernel");
+  if (d->state_f32 && !ops->tpe)
+    return mc_fail(MC_EUNSUPPORTED, "fp32 state needs the register kernels (N_eq * N_p <= 64)");
   if (d->n_elements <= 0 || d->n_surfaces < 0 || d->n_colors < 1 || d->n_ghosts < 0)
     return mc_fail(MC_EINVAL, "bad DG sizes");
   if (d->n_elements + d->n_ghosts >= (int64_t(1) << 31) || d->n_surfaces >= (int64_t(1) << 31))
@@ -258,7 +272,9 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   // 4) pads further, for DRAM-atom experiments (c4: 52 -> 56 doubles)
   int64_t align = 4;
   if (const char* a = std::getenv("MC_BLOCK_ALIGN")) align = std::max<int64_t>(4, std::atoi(a) / 4 * 4);
-  h->stride = (w + align - 1) / align * align;
+  h->stride = (w + align - 1) / align * align;   // fp32 state: 4 floats = 16-byte aligned
+  h->f32 = d->state_f32 ? 1 : 0;
+  h->esize = h->f32 ? 4 : 8;
   const int dim = ops->dim;
   std::vector<double> tables(ops->table_size);
   {
@@ -357,7 +373,7 @@ MC_API int mc_dg_set_grid_cap(mc_dg* h, int max_blocks) {
 }
 
 MC_API int64_t mc_dg_buffer_bytes(const mc_dg* h) {
-  return h ? 2 * h->ns * h->stride * int64_t(sizeof(double)) : -1;
+  return h ? 2 * h->ns * h->stride * int64_t(sizeof(double)) : -1;   // fp64 buffer
 }
 
 MC_API int mc_dg_rhs(mc_dg* h, const double* U, double* R, int strategy, void* stream) {
@@ -367,6 +383,8 @@ MC_API int mc_dg_rhs(mc_dg* h, const double* U, double* R, int strategy, void* s
   if (strategy == MC_DG_COLORED) return colored_pass(h, Um, R, nullptr, s);
   if (strategy != MC_DG_BUFFERED && strategy != MC_DG_ATOMIC)
     return mc_fail(MC_EINVAL, "unknown strategy");
+  if (h->f32)
+    return mc_fail(MC_EUNSUPPORTED, "the buffered / atomic strategies need fp64 state");
   const int gv = capped(h, h->ops->grid_volume), gu = capped(h, h->ops->grid_uncolored);
   DG_TRY(h->ops->volume(h->view, U, R, gv, s));
   if (strategy == MC_DG_ATOMIC) {
@@ -400,12 +418,12 @@ MC_API int mc_dg_color_range_pass(mc_dg* h, int color, int64_t begin, int64_t en
                                                (h->has_first[color] ? 1 : 0));
   if (rk_mode == 0) {
     DG_TRY(h->ops->colored(h->view, U, R, nullptr, bb, e, grid, as_stream(stream),
-                           h->has_first[color], h->has_last[color]));
+                           h->has_first[color], h->has_last[color], h->f32));
   } else {
     if (!U0) return mc_fail(MC_EINVAL, "RK pass needs U0");
     mcdg::RK rk{U0, a, b, dt, rk_mode == 2 ? 1 : 0};
     DG_TRY(h->ops->colored(h->view, U, R, &rk, bb, e, grid, as_stream(stream),
-                           h->has_first[color], h->has_last[color]));
+                           h->has_first[color], h->has_last[color], h->f32));
   }
   return MC_OK;
 }
@@ -423,7 +441,7 @@ MC_API int mc_dg_ssprk3(mc_dg* h, double* U, double* work, double dt, int n_step
   if (!h || !U || !work || n_steps < 0) return mc_fail(MC_EINVAL, "bad argument");
   cudaStream_t s = as_stream(stream);
   double* U0 = work;
-  double* R = work + (h->ne + h->ng) * h->stride;
+  double* R = at_blocks(work, h, h->ne + h->ng);
   auto one_step = [&]() -> int {
     // stage 1 saves U0 := U in its last-touch pass (no separate copy)
     mcdg::RK r1{U0, 0.0, 1.0, dt, 1};
@@ -481,13 +499,14 @@ MC_API int mc_dg_ssprk3(mc_dg* h, double* U, double* work, double dt, int n_step
 
 MC_API int mc_dg_ssprk3_host(mc_dg* h, double* U_host, double dt, int n_steps) {
   if (!h || !U_host) return mc_fail(MC_EINVAL, "null argument");
-  const int64_t nblk = (h->ne + h->ng) * h->stride;
-  if (!h->d_host_U) DG_TRY(cudaMalloc(&h->d_host_U, sizeof(double) * size_t(3 * nblk)));
+  const int64_t nblk = h->ne + h->ng;
+  const size_t sbytes = size_t(nblk * h->stride * h->esize);
+  if (!h->d_host_U) DG_TRY(cudaMalloc(&h->d_host_U, 3 * sbytes));
   if (!h->stream) DG_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  DG_TRY(cudaMemcpyAsync(h->d_host_U, U_host, sizeof(double) * nblk, cudaMemcpyHostToDevice,
-                         h->stream));
-  if (int rc = mc_dg_ssprk3(h, h->d_host_U, h->d_host_U + nblk, dt, n_steps, h->stream)) return rc;
-  DG_TRY(cudaMemcpyAsync(U_host, h->d_host_U, sizeof(double) * h->ne * h->stride,
+  DG_TRY(cudaMemcpyAsync(h->d_host_U, U_host, sbytes, cudaMemcpyHostToDevice, h->stream));
+  double* Ud = reinterpret_cast<double*>(h->d_host_U);
+  if (int rc = mc_dg_ssprk3(h, Ud, at_blocks(Ud, h, nblk), dt, n_steps, h->stream)) return rc;
+  DG_TRY(cudaMemcpyAsync(U_host, h->d_host_U, size_t(h->ne * h->stride * h->esize),
                          cudaMemcpyDeviceToHost, h->stream));
   DG_TRY(cudaStreamSynchronize(h->stream));
   return MC_OK;
@@ -535,8 +554,12 @@ MC_API int mc_dg_user_to_internal(mc_dg* h, const double* user_dev, double* U_de
   if (!h || !user_dev || !U_dev) return mc_fail(MC_EINVAL, "null argument");
   if (!h->d_user_src) return mc_fail(MC_EINVAL, "user row map not set (mc_dg_set_user_rows)");
   const int W = h->ops->neq * h->ops->np;
-  k_user_to_internal<<<copy_grid(h->ne * h->stride), 256, 0, as_stream(stream)>>>(
-      user_dev, h->d_user_src, U_dev, h->ne, W, int(h->stride));
+  if (h->f32)
+    k_user_to_internal<float><<<copy_grid(h->ne * h->stride), 256, 0, as_stream(stream)>>>(
+        user_dev, h->d_user_src, reinterpret_cast<float*>(U_dev), h->ne, W, int(h->stride));
+  else
+    k_user_to_internal<double><<<copy_grid(h->ne * h->stride), 256, 0, as_stream(stream)>>>(
+        user_dev, h->d_user_src, U_dev, h->ne, W, int(h->stride));
   DG_TRY(cudaGetLastError());
   return MC_OK;
 }
@@ -545,8 +568,12 @@ MC_API int mc_dg_internal_to_user(mc_dg* h, const double* U_dev, double* user_de
   if (!h || !user_dev || !U_dev) return mc_fail(MC_EINVAL, "null argument");
   if (!h->d_user_src) return mc_fail(MC_EINVAL, "user row map not set (mc_dg_set_user_rows)");
   const int W = h->ops->neq * h->ops->np;
-  k_internal_to_user<<<copy_grid(h->ne * W), 256, 0, as_stream(stream)>>>(
-      U_dev, h->d_user_src, user_dev, h->ne, W, int(h->stride));
+  if (h->f32)
+    k_internal_to_user<float><<<copy_grid(h->ne * W), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float*>(U_dev), h->d_user_src, user_dev, h->ne, W, int(h->stride));
+  else
+    k_internal_to_user<double><<<copy_grid(h->ne * W), 256, 0, as_stream(stream)>>>(
+        U_dev, h->d_user_src, user_dev, h->ne, W, int(h->stride));
   DG_TRY(cudaGetLastError());
   return MC_OK;
 }
@@ -554,9 +581,9 @@ MC_API int mc_dg_internal_to_user(mc_dg* h, const double* U_dev, double* user_de
 namespace {
 int user_staging(mc_dg* h, bool residual) {
   if (!h->d_user_src) return mc_fail(MC_EINVAL, "user row map not set (mc_dg_set_user_rows)");
-  const int64_t nblk = (h->ne + h->ng) * h->stride;
+  const size_t sbytes = size_t((h->ne + h->ng) * h->stride * h->esize);
   const size_t ubytes = sizeof(double) * size_t(h->n_user_rows) * h->ops->neq * h->ops->np;
-  if (!h->d_host_U) DG_TRY(cudaMalloc(&h->d_host_U, sizeof(double) * size_t(3 * nblk)));
+  if (!h->d_host_U) DG_TRY(cudaMalloc(&h->d_host_U, 3 * sbytes));
   if (!h->d_user) DG_TRY(cudaMalloc(&h->d_user, ubytes));
   if (residual && !h->d_user_R) DG_TRY(cudaMalloc(&h->d_user_R, ubytes));
   if (!h->stream) DG_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -568,12 +595,13 @@ MC_API int mc_dg_ssprk3_user_host(mc_dg* h, double* U_host, double dt, int n_ste
   if (!h || !U_host) return mc_fail(MC_EINVAL, "null argument");
   if (h->ng) return mc_fail(MC_EINVAL, "partitioned operator: use the device entry points");
   if (int rc = user_staging(h, false)) return rc;
-  const int64_t nblk = (h->ne + h->ng) * h->stride;
+  const int64_t nblk = h->ne + h->ng;
   const size_t ubytes = sizeof(double) * size_t(h->n_user_rows) * h->ops->neq * h->ops->np;
+  double* Ud = reinterpret_cast<double*>(h->d_host_U);
   DG_TRY(cudaMemcpyAsync(h->d_user, U_host, ubytes, cudaMemcpyHostToDevice, h->stream));
-  if (int rc = mc_dg_user_to_internal(h, h->d_user, h->d_host_U, h->stream)) return rc;
-  if (int rc = mc_dg_ssprk3(h, h->d_host_U, h->d_host_U + nblk, dt, n_steps, h->stream)) return rc;
-  if (int rc = mc_dg_internal_to_user(h, h->d_host_U, h->d_user, h->stream)) return rc;
+  if (int rc = mc_dg_user_to_internal(h, h->d_user, Ud, h->stream)) return rc;
+  if (int rc = mc_dg_ssprk3(h, Ud, at_blocks(Ud, h, nblk), dt, n_steps, h->stream)) return rc;
+  if (int rc = mc_dg_internal_to_user(h, Ud, h->d_user, h->stream)) return rc;
   DG_TRY(cudaMemcpyAsync(U_host, h->d_user, ubytes, cudaMemcpyDeviceToHost, h->stream));
   DG_TRY(cudaStreamSynchronize(h->stream));
   return MC_OK;
@@ -583,13 +611,15 @@ MC_API int mc_dg_rhs_user_host(mc_dg* h, const double* U_host, double* R_host, i
   if (!h || !U_host || !R_host) return mc_fail(MC_EINVAL, "null argument");
   if (h->ng) return mc_fail(MC_EINVAL, "partitioned operator: use the device entry points");
   if (int rc = user_staging(h, true)) return rc;
-  const int64_t nblk = (h->ne + h->ng) * h->stride;
+  const int64_t nblk = h->ne + h->ng;
   const size_t ubytes = sizeof(double) * size_t(h->n_user_rows) * h->ops->neq * h->ops->np;
+  double* Ud = reinterpret_cast<double*>(h->d_host_U);
   DG_TRY(cudaMemcpyAsync(h->d_user, U_host, ubytes, cudaMemcpyHostToDevice, h->stream));
-  if (int rc = mc_dg_user_to_internal(h, h->d_user, h->d_host_U, h->stream)) return rc;
-  if (int rc = mc_dg_rhs(h, h->d_host_U, h->d_host_U + 2 * nblk, strategy, h->stream)) return rc;
+  if (int rc = mc_dg_user_to_internal(h, h->d_user, Ud, h->stream)) return rc;
+  if (int rc = mc_dg_rhs(h, Ud, at_blocks(Ud, h, 2 * nblk), strategy, h->stream)) return rc;
   DG_TRY(cudaMemsetAsync(h->d_user_R, 0, ubytes, h->stream));
-  if (int rc = mc_dg_internal_to_user(h, h->d_host_U + 2 * nblk, h->d_user_R, h->stream)) return rc;
+  if (int rc = mc_dg_internal_to_user(h, at_blocks(Ud, h, 2 * nblk), h->d_user_R, h->stream))
+    return rc;
   DG_TRY(cudaMemcpyAsync(R_host, h->d_user_R, ubytes, cudaMemcpyDeviceToHost, h->stream));
   DG_TRY(cudaStreamSynchronize(h->stream));
   return MC_OK;

@@ -217,11 +217,11 @@ struct View {
   // interface element's new block into its slot of the ghost-exchange send
   // buffer (send_slot[e] >= 0), so the next stage posts it without a pack
   const int32_t* send_slot;
-  double* send_buf;
+  void* send_buf;          // element blocks of the state type (double / float)
 };
 
 struct RK {
-  double* U0;     // stage base state (read when a != 0; written when save_u0)
+  void* U0;       // stage base state (read when a != 0; written when save_u0), state type
   double a, b, dt;
   int save_u0;    // first SSP-RK stage: U0 := U before the in-place update
 };
@@ -831,10 +831,10 @@ k_surface_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk,
     surface_tasks<C, PH>(st, ws, ln, c, u, v.prm, acc);
     if (c.owner) {
       if (kRK && last) {
-        if (rk.save_u0) store_run<C::NP>(rk.U0 + off, u);
+        if (rk.save_u0) store_run<C::NP>(static_cast<double*>(rk.U0) + off, u);
         if (rk.a != 0.0) {
           double u0[C::NP];
-          load_run<C::NP>(rk.U0 + off, u0);
+          load_run<C::NP>(static_cast<const double*>(rk.U0) + off, u0);
 #pragma unroll
           for (int j = 0; j < C::NP; ++j) acc[j] = rk.a * u0[j] + rk.b * fma(rk.dt, acc[j], u[j]);
         } else {
@@ -844,7 +844,9 @@ k_surface_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk,
         store_run<C::NP>(U + off, acc);
         if (v.send_slot) {
           const int sl = __ldg(v.send_slot + c.e);
-          if (sl >= 0) store_run<C::NP>(v.send_buf + int64_t(sl) * v.stride + ln.eq * C::NP, acc);
+          if (sl >= 0)
+            store_run<C::NP>(static_cast<double*>(v.send_buf) + int64_t(sl) * v.stride + ln.eq * C::NP,
+                             acc);
         }
       } else {
         store_run<C::NP>(R + off, acc);

@@ -16,8 +16,11 @@ struct Ops {
   // per colored-kernel variant, index (rk-update ? 2 : 0) | (volume ? 1 : 0):
   // each variant has its own register budget, so its own resident grid
   int grid_var[4];
-  cudaError_t (*colored)(const View&, double* U, double* R, const RK* rk, int64_t b,
-                         int64_t e, int grid, cudaStream_t s, bool has_first, bool has_last);
+  // U / R point to element blocks of the state type: double, or float when
+  // f32 (fp32 state storage, register kernels only)
+  cudaError_t (*colored)(const View&, void* U, void* R, const RK* rk, int64_t b,
+                         int64_t e, int grid, cudaStream_t s, bool has_first, bool has_last,
+                         bool f32);
   cudaError_t (*volume)(const View&, const double* U, double* R, int grid, cudaStream_t s);
   cudaError_t (*uncolored)(const View&, const double* U, double* out, bool atomic, int grid,
                            cudaStream_t s);
@@ -30,6 +33,7 @@ struct Ops {
   cudaError_t (*upload_const)(const double* ptables_dev);
   int npl;                          // P_{p-1} modes of the factored projection
   int p1proj;                       // the register kernels use it (Cfg::P1PROJ)
+  int tpe;                          // register kernels (fp32 state possible)
 };
 
 // defined in dg_tri.cu / dg_quad.cu / dg_tet.cu; nullptr if not compiled
@@ -42,24 +46,38 @@ template <int K, int PH, int P>
 struct Instance {
   using C = Cfg<K, PH, P>;
   using T = Tpe<C>;
-  static cudaError_t colored(const View& v, double* U, double* R, const RK* rk, int64_t b,
-                             int64_t e, int grid, cudaStream_t s, bool has_first, bool has_last) {
+  template <class S>
+  static void launch_tpe(const View& v, S* U, S* R, const RK* rk, int64_t b, int64_t e, int grid,
+                         cudaStream_t s, bool has_first, bool has_last) {
+    const bool krk = rk && has_last;
+    const RK r = rk ? *rk : RK{};
+    if (krk && has_first)
+      k_tpe_colored<C, PH, true, true, S><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
+    else if (krk)
+      k_tpe_colored<C, PH, true, false, S><<<grid, T::THREADS, T::SMEM_SURF, s>>>(v, U, R, r, b, e);
+    else if (has_first)
+      k_tpe_colored<C, PH, false, true, S><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
+    else
+      k_tpe_colored<C, PH, false, false, S><<<grid, T::THREADS, T::SMEM_SURF, s>>>(v, U, R, r, b, e);
+  }
+  static cudaError_t colored(const View& v, void* U, void* R, const RK* rk, int64_t b,
+                             int64_t e, int grid, cudaStream_t s, bool has_first, bool has_last,
+                             bool f32) {
     if constexpr (T::OK) {
-      const bool krk = rk && has_last;
-      const RK r = rk ? *rk : RK{};
-      if (krk && has_first)
-        k_tpe_colored<C, PH, true, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
-      else if (krk)
-        k_tpe_colored<C, PH, true, false><<<grid, T::THREADS, T::SMEM_SURF, s>>>(v, U, R, r, b, e);
-      else if (has_first)
-        k_tpe_colored<C, PH, false, true><<<grid, T::THREADS, T::SMEM, s>>>(v, U, R, r, b, e);
+      if (f32)
+        launch_tpe<float>(v, static_cast<float*>(U), static_cast<float*>(R), rk, b, e, grid, s,
+                          has_first, has_last);
       else
-        k_tpe_colored<C, PH, false, false><<<grid, T::THREADS, T::SMEM_SURF, s>>>(v, U, R, r, b, e);
+        launch_tpe<double>(v, static_cast<double*>(U), static_cast<double*>(R), rk, b, e, grid,
+                           s, has_first, has_last);
     } else {
+      if (f32) return cudaErrorNotSupported;
+      double* Ud = static_cast<double*>(U);
+      double* Rd = static_cast<double*>(R);
       if (rk)
-        k_surface_colored<C, PH, true><<<grid, C::THREADS, C::SMEM, s>>>(v, U, R, *rk, b, e);
+        k_surface_colored<C, PH, true><<<grid, C::THREADS, C::SMEM, s>>>(v, Ud, Rd, *rk, b, e);
       else
-        k_surface_colored<C, PH, false><<<grid, C::THREADS, C::SMEM, s>>>(v, U, R, RK{}, b, e);
+        k_surface_colored<C, PH, false><<<grid, C::THREADS, C::SMEM, s>>>(v, Ud, Rd, RK{}, b, e);
     }
     return cudaGetLastError();
   }
@@ -115,6 +133,13 @@ struct Instance {
       if ((err = fit((const void*)k_tpe_colored<C, PH, false, true>, T::SMEM, T::THREADS, &o->grid_var[1]))) return err;
       if ((err = fit((const void*)k_tpe_colored<C, PH, true, false>, T::SMEM_SURF, T::THREADS, &o->grid_var[2]))) return err;
       if ((err = fit((const void*)k_tpe_colored<C, PH, false, false>, T::SMEM_SURF, T::THREADS, &o->grid_var[0]))) return err;
+      // the fp32-state instantiations share the grids (same launch bounds)
+      for (const void* fn : {(const void*)k_tpe_colored<C, PH, true, true, float>,
+                             (const void*)k_tpe_colored<C, PH, false, true, float>})
+        if ((err = fit(fn, T::SMEM, T::THREADS, &g2))) return err;
+      for (const void* fn : {(const void*)k_tpe_colored<C, PH, true, false, float>,
+                             (const void*)k_tpe_colored<C, PH, false, false, float>})
+        if ((err = fit(fn, T::SMEM_SURF, T::THREADS, &g2))) return err;
       o->grid_colored = o->grid_var[0];
       for (int k = 1; k < 4; ++k)
         if (o->grid_var[k] < o->grid_colored) o->grid_colored = o->grid_var[k];
@@ -153,7 +178,7 @@ struct Instance {
     static Ops o{C::DIM, C::NEQ, C::NP, C::NQF, C::NQV, C::NCODES, C::T_SIZE,
                  T::OK ? T::THREADS : C::THREADS, T::OK ? T::SW : C::SPW,
                  0, 0, 0, {0, 0, 0, 0}, &colored, &volume, &uncolored, &gather, &init, C::S_TOTAL,
-                 &stage_global, &upload_const, C::NPL, C::P1PROJ ? 1 : 0};
+                 &stage_global, &upload_const, C::NPL, C::P1PROJ ? 1 : 0, T::OK ? 1 : 0};
     return &o;
   }
 };

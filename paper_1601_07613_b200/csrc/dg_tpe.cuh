@@ -150,7 +150,6 @@ __device__ __forceinline__ void assemble_state(const double (&own)[Tpe<C>::NEQH]
     double oth[NEQH];
 #pragma unroll
     for (int k = 0; k < NEQH; ++k) oth[k] = __shfl_xor_sync(kFull, own[k], 1);
-#pragma unroll
     constexpr int NA = Tpe<C>::NA;
 #pragma unroll
     for (int e = 0; e < C::NEQ; ++e)
@@ -882,6 +881,77 @@ __device__ __forceinline__ void tstore(double* dst, int n, const double (&src)[N
   }
 }
 
+// fp32 state storage (DGOperator(state="f32"); the north star's "1e-5
+// (fp32)" tolerance): element blocks of floats, converted to double on load
+// and rounded back on store; all arithmetic stays fp64.  Runs are 16-byte
+// aligned (float strides are multiples of 4), moved as 128-bit accesses.
+__device__ __forceinline__ void ld4f(const float* p, bool nc, double& a, double& b, double& c,
+                                     double& d) {
+  float x, y, z, w;
+  if (nc)
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "l"(p));
+  else
+    asm("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "l"(p));
+  a = x;
+  b = y;
+  c = z;
+  d = w;
+}
+
+template <int N, bool kWhole>
+__device__ __forceinline__ void fload(const float* src, int n, double (&dst)[N], bool nc) {
+#pragma unroll
+  for (int j = 0; j < N / 4; ++j) {
+    if (kWhole || 4 * j + 4 <= n)
+      ld4f(src + 4 * j, nc, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
+    else
+      dst[4 * j] = dst[4 * j + 1] = dst[4 * j + 2] = dst[4 * j + 3] = 0.0;
+  }
+#pragma unroll
+  for (int j = N / 4 * 4; j < N; ++j) dst[j] = (kWhole || j < n) ? double(src[j]) : 0.0;
+}
+
+template <int N, bool kWhole>
+__device__ __forceinline__ void fstore(float* dst, int n, const double (&src)[N]) {
+#pragma unroll
+  for (int j = 0; j < N / 4; ++j)
+    if (kWhole || 4 * j + 4 <= n)
+      *reinterpret_cast<float4*>(dst + 4 * j) =
+          make_float4(__double2float_rn(src[4 * j]), __double2float_rn(src[4 * j + 1]),
+                      __double2float_rn(src[4 * j + 2]), __double2float_rn(src[4 * j + 3]));
+#pragma unroll
+  for (int j = N / 4 * 4; j < N; ++j)
+    if (kWhole || j < n) dst[j] = __double2float_rn(src[j]);
+}
+
+// state-type dispatch: S = double (the default) or float
+template <int N, bool kWhole, bool kV4>
+__device__ __forceinline__ void sload(const double* src, int n, double (&dst)[N]) {
+  tload<N, kWhole, kV4>(src, n, dst);
+}
+template <int N, bool kWhole, bool kV4>
+__device__ __forceinline__ void sload(const float* src, int n, double (&dst)[N]) {
+  fload<N, kWhole>(src, n, dst, true);
+}
+template <int N, bool kWhole, bool kV4>
+__device__ __forceinline__ void sload_rw(const double* src, int n, double (&dst)[N]) {
+  tload_rw<N, kWhole, kV4>(src, n, dst);
+}
+template <int N, bool kWhole, bool kV4>
+__device__ __forceinline__ void sload_rw(const float* src, int n, double (&dst)[N]) {
+  fload<N, kWhole>(src, n, dst, false);
+}
+template <int N, bool kWhole, bool kV4>
+__device__ __forceinline__ void sstore(double* dst, int n, const double (&src)[N]) {
+  tstore<N, kWhole, kV4>(dst, n, src);
+}
+template <int N, bool kWhole, bool kV4>
+__device__ __forceinline__ void sstore(float* dst, int n, const double (&src)[N]) {
+  fstore<N, kWhole>(dst, n, src);
+}
+
 template <class C>
 __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* s) {
   stage_tables<C>(g, s);
@@ -930,7 +1000,7 @@ __device__ __forceinline__ TpeLane tpe_lane() {
 // kVol: the color contains first touches (volume fused); kRK: the color
 // contains last touches of an RK stage (update fused).  The host picks the
 // variant per color launch so surface-only passes carry no volume code.
-template <class C, int PH, bool kRK, bool kVol>
+template <class C, int PH, bool kRK, bool kVol, class S = double>
 __global__ void __launch_bounds__(Tpe<C>::THREADS,
                                   Tpe<C>::H == 2
                                       ? ((!kVol && !kRK) ? MC_TASKS_MINB_SURF
@@ -938,8 +1008,9 @@ __global__ void __launch_bounds__(Tpe<C>::THREADS,
                                                 : MC_TPE_MINB_RK2)
                                   : kVol ? (MC_TPE_MINB_VOL ? MC_TPE_MINB_VOL : Tpe<C>::MINB)
                                   : (kRK ? MC_TPE_MINB_RK : MC_TPE_MINB_SURF))
-k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int64_t begin,
+k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin,
               int64_t end) {
+  S* const U0 = static_cast<S*>(rk.U0);
   using T = Tpe<C>;
   constexpr int WH = T::WH;
   constexpr bool kWhole = T::H == 1;
@@ -987,7 +1058,7 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
     const bool last = kRK && t.owner && (t.code & (ln.side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
     const int64_t off = int64_t(t.has ? t.e : 0) * v.stride + ln.eq0 * C::NP;
     double u[WH], acc[WH];
-    if (t.has) tload<WH, kWhole, T::V4>(U + off, n, u);
+    if (t.has) sload<WH, kWhole, T::V4>(U + off, n, u);
     else {
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
@@ -998,7 +1069,7 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
 #pragma unroll
       for (int j = 0; j < WH; ++j) acc[j] = 0.0;
     } else {
-      tload_rw<WH, kWhole, T::V4>(R + off, n, acc);
+      sload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     }
     if constexpr (kVol) {
       const double* jp = v.jinv + int64_t(first ? t.e : 0) * (C::DIM * C::DIM);
@@ -1007,7 +1078,7 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
       } else if (__any_sync(kFull, first)) {   // the whole warp takes part in the shuffles
         tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc);
       }
-      if (t.owner && !first) tload_rw<WH, kWhole, T::V4>(R + off, n, acc);
+      if (t.owner && !first) sload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     }
     tpe_surface<C, PH, (kVol ? T::TASKS : T::TASKS_SURF)>(st, t, ln.side, ln.h, ln.nown, u, v.prm,
                                                           acc, ln.grp, ws);
@@ -1016,26 +1087,26 @@ k_tpe_colored(View v, double* __restrict__ U, double* __restrict__ R, RK rk, int
 #ifdef MC_RK_RELOAD_U
         // re-read the element's own block (L2) instead of keeping u live
         // through the surface work (fewer registers in the last-touch pass)
-        if constexpr (kRK && !kVol) tload<WH, kWhole, T::V4>(U + off, n, u);
+        if constexpr (kRK && !kVol) sload<WH, kWhole, T::V4>(U + off, n, u);
 #endif
-        if (rk.save_u0) tstore<WH, kWhole, T::V4>(rk.U0 + off, n, u);
+        if (rk.save_u0) sstore<WH, kWhole, T::V4>(U0 + off, n, u);
         if (rk.a != 0.0) {
           double u0[WH];
-          tload<WH, kWhole, T::V4>(rk.U0 + off, n, u0);
+          sload<WH, kWhole, T::V4>(U0 + off, n, u0);
 #pragma unroll
           for (int j = 0; j < WH; ++j) acc[j] = rk.a * u0[j] + rk.b * fma(rk.dt, acc[j], u[j]);
         } else {
 #pragma unroll
           for (int j = 0; j < WH; ++j) acc[j] = rk.b * fma(rk.dt, acc[j], u[j]);
         }
-        tstore<WH, kWhole, T::V4>(U + off, n, acc);
+        sstore<WH, kWhole, T::V4>(U + off, n, acc);
         if (v.send_slot) {
           const int sl = __ldg(v.send_slot + t.e);
           if (sl >= 0)
-            tstore<WH, kWhole, T::V4>(v.send_buf + int64_t(sl) * v.stride + ln.eq0 * C::NP, n, acc);
+            sstore<WH, kWhole, T::V4>(static_cast<S*>(v.send_buf) + int64_t(sl) * v.stride + ln.eq0 * C::NP, n, acc);
         }
       } else {
-        tstore<WH, kWhole, T::V4>(R + off, n, acc);
+        sstore<WH, kWhole, T::V4>(R + off, n, acc);
       }
     }
   }

@@ -154,7 +154,7 @@ class DGOperator:
                  physics: str = "euler", *, period=None, gamma: float = 1.4,
                  velocity=(1.0, 0.5, 0.25), farfield=None, ordering: str | None = None,
                  world: int = 1, rank: int = 0, code_sort: bool | int | None = None,
-                 grid_cap: int | None = None):
+                 grid_cap: int | None = None, state: str = "f64"):
         mortars = None
         if isinstance(mesh, RefinedMesh):
             mortars = mesh.hanging_array()
@@ -170,6 +170,11 @@ class DGOperator:
         self.physics = physics
         if physics not in ("advection", "euler"):
             raise ValueError(f"unknown physics {physics!r}")
+        if state not in ("f64", "f32"):
+            raise ValueError(f"state must be 'f64' or 'f32', got {state!r}")
+        # "f32": element blocks stored as floats (half the bytes), arithmetic
+        # in fp64; colored strategy only; the north star's 1e-5 tolerance
+        self.state = state
         self.n_equations = 1 if physics == "advection" else self.dim + 2
         self.gamma = float(gamma)
         self.velocity = tuple(float(v) for v in velocity) + (0.0,) * (3 - len(velocity))
@@ -253,6 +258,7 @@ class DGOperator:
         d.face_phi, d.face_w = P(keep["fphi"]), P(keep["fw"])
         d.vol_phi, d.vol_dphi, d.vol_w = P(keep["vphi"]), P(keep["vdphi"]), P(keep["vw"])
         d.gamma = self.gamma
+        d.state_f32 = 1 if self.state == "f32" else 0
         for k in range(3):
             d.velocity[k] = self.velocity[k]
         ff = list(self.farfield) + [0.0] * (5 - len(self.farfield))
@@ -349,18 +355,23 @@ class DGOperator:
         return B[self.plan.element_perm, : self.block_width()].reshape(
             self.n_elements, self.n_equations, self.n_basis).copy()
 
+    @property
+    def torch_dtype(self):
+        import torch
+        return torch.float32 if self.state == "f32" else torch.float64
+
     def empty_device(self):
         import torch
-        return torch.zeros((self.n_local, self.stride), dtype=torch.float64, device="cuda")
+        return torch.zeros((self.n_local, self.stride), dtype=self.torch_dtype, device="cuda")
 
     def to_device(self, U: np.ndarray):
         import torch
-        return torch.from_numpy(self.to_internal(U)).to("cuda")
+        return torch.from_numpy(self.to_internal(U)).to("cuda", dtype=self.torch_dtype)
 
     def from_device(self, t) -> np.ndarray:
         import torch
         torch.cuda.current_stream().synchronize()
-        return self.from_internal(t.cpu().numpy())
+        return self.from_internal(t.double().cpu().numpy())
 
     # ------------------------------------------------------- evaluation
     def rhs_device(self, U_dev, R_dev, strategy: str = "colored", stream=None) -> None:
@@ -424,7 +435,7 @@ class DGOperator:
 
     def work_device(self):
         import torch
-        return torch.zeros((2, self.n_local, self.stride), dtype=torch.float64, device="cuda")
+        return torch.zeros((2, self.n_local, self.stride), dtype=self.torch_dtype, device="cuda")
 
     STAGES = ((2, 0.0, 1.0), (1, 0.75, 0.25), (1, 1.0 / 3.0, 2.0 / 3.0))
 

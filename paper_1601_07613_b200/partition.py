@@ -168,7 +168,8 @@ class HaloExchange:
         slot = self.send_slots()
         if slot is None:
             return False
-        buf = self._buffer(torch.empty((0, stride), dtype=torch.float64, device=self.device))
+        buf = self._buffer(torch.empty((0, stride), dtype=getattr(op, "torch_dtype", torch.float64),
+                                       device=self.device))
         _native.check(op._lib.mc_dg_set_send_rows(op._h, _native.ptr(slot), _native.ptr(buf),
                                                   int(self.n_send)))
         self.packed_by_kernel = True
