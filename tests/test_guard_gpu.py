@@ -95,4 +95,5 @@ def test_send_buffer_packing_stays_inside(cuda):
     assert guards_intact(big, h.n_send)
     rows = torch.as_tensor(h.rows, device="cuda")
     assert torch.isfinite(U).all()
-    assert torch.equal(buf[: h.n_send], U.index_select(0, rows))
+    W = op.block_width()                     # the padding of send rows is never written
+    assert torch.equal(buf[: h.n_send, :W], U.index_select(0, rows)[:, :W])
