@@ -295,9 +295,14 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (
         for (int k = 0; k < NEQH; ++k) {
           const double fm = own_part<C>(F + d * NEQ, h, k);
           const double fr = __shfl_xor_sync(kFull, own_part<C>(F + d * NEQ, h ^ 1, k), 1);
+#ifdef MC_PAIR_NO_ON   // no zeroing: garbage stays in non-contributing lane pairs
+          const double f0 = h ? fr : fm;
+          const double f1 = h ? fm : fr;
+#else
           const bool on = mine && k < nown;
           const double f0 = on ? (h ? fr : fm) : 0.0;
           const double f1 = on ? (h ? fm : fr) : 0.0;
+#endif
 #pragma unroll
           for (int m = 0; m < M; ++m)
             Pm[d][k][m] = fma(wpsi[q1 * M + m], f1, fma(wpsi[q0 * M + m], f0, Pm[d][k][m]));
