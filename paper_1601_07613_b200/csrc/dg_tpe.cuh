@@ -985,6 +985,19 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 #define MC_TPE_MINB_VOL2 3  // two lanes per side, first-touch passes (tets)
 #endif
 
+// surface-flux scheme per kernel variant: warp flux tasks (Tpe::TASKS /
+// TASKS_SURF) or each lane's own flux; MC_RK_NO_TASKS / MC_VOL_NO_TASKS
+// switch the last-touch / first-touch variants to per-lane fluxes (A/B)
+template <class T, bool kRK, bool kVol>
+constexpr bool kVariantTasks =
+#if defined(MC_VOL_NO_TASKS)
+    kVol ? false :
+#endif
+#if defined(MC_RK_NO_TASKS)
+    (kRK && !kVol) ? false :
+#endif
+    (kVol ? T::TASKS : T::TASKS_SURF);
+
 struct TpeLane {
   int lane, side, h, grp, nown, eq0;
 };
@@ -1085,8 +1098,8 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
       }
       if (t.owner && !first) sload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     }
-    tpe_surface<C, PH, (kVol ? T::TASKS : T::TASKS_SURF)>(st, t, ln.side, ln.h, ln.nown, u, v.prm,
-                                                          acc, ln.grp, ws);
+    tpe_surface<C, PH, kVariantTasks<T, kRK, kVol>>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc,
+                                                     ln.grp, ws);
     if (t.owner) {
       if (last) {
 #ifdef MC_RK_RELOAD_U
