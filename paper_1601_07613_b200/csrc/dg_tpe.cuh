@@ -250,7 +250,11 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (
     for (int q = 0; q < C::NQV; ++q) point(q);
   } else {
     constexpr int NA = Tpe<C>::NA;
-#pragma unroll 1
+#ifndef MC_PAIR_UNROLL
+#define MC_PAIR_UNROLL 1
+#endif
+    constexpr int kPairUnroll = MC_PAIR_UNROLL;
+#pragma unroll kPairUnroll
     for (int q0 = 0; q0 + 1 < C::NQV; q0 += 2) {
       const int q1 = q0 + 1;
       double mt[NEQH], ot[NEQH];
