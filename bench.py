@@ -382,9 +382,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # MC_DIST_BACKEND=gloo: functional run of the N>1 path with host-staged
+    # exchanges (e.g. several ranks on one GPU to exercise the code); never a
+    # measurement — the scaling numbers are NCCL over NVLink, one rank per GPU
+    backend = os.environ.get("MC_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local % torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def reduce_scalar(x, op):
+        t = torch.tensor([x], device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=op)
+        return float(t.item())
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
 
@@ -395,9 +407,7 @@ def main():
     U_host = op.initial_state("wave")
     dt = op.stable_dt(0.2)
     if world > 1:                      # one global time step; also initialises NCCL P2P
-        t = torch.tensor([dt], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        dt = float(t.item())
+        dt = reduce_scalar(dt, dist.ReduceOp.MIN)
         dist.barrier()
     U = op.to_device(U_host)
     work = op.work_device()
@@ -443,9 +453,7 @@ def main():
     barrier()
     total_ms = start.elapsed_time(end)
     if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = reduce_scalar(total_ms, dist.ReduceOp.MAX)
     ms_per_step = total_ms / max(args.steps, 1)
     ns_global = op.n_surfaces if world == 1 else op.mesh.n_surfaces
     ne_global = op.mesh.n_elements
@@ -509,9 +517,7 @@ def main():
             torch.cuda.synchronize()
         barrier()
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = reduce_scalar(e2e_s, dist.ReduceOp.MAX)
         io_bytes = own * W * 8 * world
     e2e_value = 3 * ns_global / e2e_s
 
@@ -548,7 +554,8 @@ def main():
                          f"{op.n_local * op.stride * (4 if args.state == 'f32' else 8) / 1e9:.2f}"
                          " GB x 3 arrays, no flush needed)",
                    "parallelism": "single-GPU" if world == 1 else
-                   f"domain decomposition x{world} (slabs, NCCL ghost exchange per stage)",
+                   f"domain decomposition x{world} (slabs, {backend.upper()} ghost exchange per "
+                   f"stage{'' if backend == 'nccl' else ', host-staged: functional run only'})",
                    "setup_s": round(t_setup, 2)},
         "dof_updates_per_s": dof_rate,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

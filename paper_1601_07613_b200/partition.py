@@ -190,20 +190,30 @@ class HaloExchange:
         if not self.fresh and self.n_send:
             torch.index_select(U, 0, self.send_idx, out=buf[: self.n_send])
         self.fresh = False
-        ops = []
+        # a CPU backend (gloo) with device tensors: stage through host memory
+        staged = U.is_cuda and dist.get_backend() != "nccl"
+        if staged:
+            buf = buf.cpu()
+        ops, landing = [], []
         for q in self.peers:
             a, b = self.offs[q]
             ops.append(dist.P2POp(dist.isend, buf[a:b], q))
         for q, (a, b) in self.part.recv.items():
-            ops.append(dist.P2POp(dist.irecv, U[a:b], q))
+            dst = torch.empty((b - a,) + tuple(U.shape[1:]), dtype=U.dtype) if staged else U[a:b]
+            landing.append((a, b, dst))
+            ops.append(dist.P2POp(dist.irecv, dst, q))
         reqs = dist.batch_isend_irecv(ops) if ops else []
-        return reqs
+        return reqs, (landing if staged else None), buf
 
     def finish(self, U, handle) -> None:
         """Wait for the transfers (with NCCL the current stream waits, not
-        the host); the ghost rows are already in place."""
-        for req in handle:
+        the host); the ghost rows are already in place (host-staged
+        backends: copied in here)."""
+        reqs, landing, _buf = handle
+        for req in reqs:
             req.wait()
+        for a, b, dst in landing or ():
+            U[a:b].copy_(dst)
 
     def exchange(self, U) -> None:
         self.finish(U, self.start(U))
