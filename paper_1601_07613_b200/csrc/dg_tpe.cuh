@@ -622,15 +622,35 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
     }
 #pragma unroll 1
     for (int g = 0; g < C::NQF; ++g) {
+#ifndef MC_TRACE_ROW_RELOAD
+      // the face-table row once per point, shared by the lane's equations
+      // (read per equation it was half of all shared-memory wavefronts of
+      // the c4 surface passes, ncu r2c4b)
+      double row[C::NPP];
+      {
+        const double2* r2 = reinterpret_cast<const double2*>(fphi + g * C::NPP);
+#pragma unroll
+        for (int j = 0; j < C::NPP / 2; ++j) {
+          const double2 a = r2[j];
+          row[2 * j] = a.x;
+          row[2 * j + 1] = a.y;
+        }
+      }
+#endif
 #pragma unroll
       for (int k = 0; k < NEQH; ++k) {
         if (k < nown) {
-          // MC_TRACE_ILP: two half-length FMA chains (c4 surface colors -6 %
-          // at the 168-register budget of 3 blocks per SM)
-#ifndef MC_TRACE_ILP
+#ifndef MC_TRACE_ROW_RELOAD
+          double tv = 0.0;
+#pragma unroll
+          for (int j = 0; j < NP; ++j) tv = fma(row[j], u[k * NP + j], tv);
+          const double v = t.has ? tv : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
+#elif !defined(MC_TRACE_ILP)
           const double v = t.has ? tdot<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP)
                                  : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
 #else
+          // two half-length FMA chains (c4 surface colors -6 % at the
+          // 168-register budget of 3 blocks per SM)
           const double v = t.has ? tdot2<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP)
                                  : ((t.valid && side) ? P.ff[eq0 + k] : 1.0);
 #endif
@@ -672,11 +692,31 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
 #pragma unroll 1
       for (int g = 0; g < C::NQF; ++g) {
         const double c = sc2 * fw[g];
+#ifndef MC_TRACE_ROW_RELOAD
+        double row[C::NPP];
+        {
+          const double2* r2 = reinterpret_cast<const double2*>(fphi + g * C::NPP);
+#pragma unroll
+          for (int j = 0; j < C::NPP / 2; ++j) {
+            const double2 a = r2[j];
+            row[2 * j] = a.x;
+            row[2 * j + 1] = a.y;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NEQH; ++k)
+          if (k < nown) {
+            const double f = c * fs[(g * SW + grp) * SV + eq0 + k];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) acc[k * NP + j] = fma(row[j], f, acc[k * NP + j]);
+          }
+#else
 #pragma unroll
         for (int k = 0; k < NEQH; ++k)
           if (k < nown)
             taxpy<NP, Tpe<C>::WH>(fphi + g * C::NPP, c * fs[(g * SW + grp) * SV + eq0 + k], acc,
                                   k * NP);
+#endif
       }
     }
     __syncwarp();
@@ -684,10 +724,33 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
     double trc[C::NQF][NEQH];
 #pragma unroll
     for (int g = 0; g < C::NQF; ++g) {
+#if defined(MC_H1_ROW_ONCE) && !defined(MC_TRACE_ROW_RELOAD)
+      // the table row once per point, not once per equation (opt-in for one
+      // lane per side: the fully unrolled point loop then keeps every row
+      // live and the RK variants spill 520 bytes at c2's register budget)
+      double row[C::NPP];
+      {
+        const double2* r2 = reinterpret_cast<const double2*>(fphi + g * C::NPP);
+#pragma unroll
+        for (int j = 0; j < C::NPP / 2; ++j) {
+          const double2 a = r2[j];
+          row[2 * j] = a.x;
+          row[2 * j + 1] = a.y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k) {
+        double tv = 0.0;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) tv = fma(row[j], u[k * NP + j], tv);
+        trc[g][k] = t.has ? tv : ((t.valid && side) ? P.ff[k] : 1.0);   // far-field ghost
+      }
+#else
 #pragma unroll
       for (int k = 0; k < NEQH; ++k)
         trc[g][k] = t.has ? tdot<NP, Tpe<C>::WH>(fphi + g * C::NPP, u, k * NP)
                           : ((t.valid && side) ? P.ff[k] : 1.0);   // far-field ghost
+#endif
     }
 #pragma unroll
     for (int g = 0; g < C::NQF; ++g) {
@@ -701,8 +764,27 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
 #endif
       if (t.owner) {
         const double c = sc * fw[g];
+#if defined(MC_H1_ROW_ONCE) && !defined(MC_TRACE_ROW_RELOAD)
+        double row[C::NPP];
+        {
+          const double2* r2 = reinterpret_cast<const double2*>(fphi + g * C::NPP);
+#pragma unroll
+          for (int j = 0; j < C::NPP / 2; ++j) {
+            const double2 a = r2[j];
+            row[2 * j] = a.x;
+            row[2 * j + 1] = a.y;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NEQ; ++k) {
+          const double f = c * out[k];
+#pragma unroll
+          for (int j = 0; j < NP; ++j) acc[k * NP + j] = fma(row[j], f, acc[k * NP + j]);
+        }
+#else
 #pragma unroll
         for (int k = 0; k < NEQ; ++k) taxpy<NP, Tpe<C>::WH>(fphi + g * C::NPP, c * out[k], acc, k * NP);
+#endif
       }
     }
   } else {
