@@ -1161,6 +1161,15 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
     const bool first = kVol && t.owner && (t.code & (ln.side ? MC_FLAG_R_FIRST : MC_FLAG_L_FIRST));
     const bool last = kRK && t.owner && (t.code & (ln.side ? MC_FLAG_R_LAST : MC_FLAG_L_LAST));
     const int64_t off = int64_t(t.has ? t.e : 0) * v.stride + ln.eq0 * C::NP;
+#ifdef MC_U0_PREFETCH
+    // last-touch passes: pull the RK base block into L1 now, read it at the end
+    if (kRK && last && rk.a != 0.0) {
+      const char* p0 = reinterpret_cast<const char*>(U0 + off);
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p0));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p0 + 128));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p0 + n * sizeof(S) - 1));
+    }
+#endif
     double u[WH], acc[WH];
     if (t.has) sload<WH, kWhole, T::V4>(U + off, n, u);
     else {
