@@ -197,15 +197,22 @@ class DGOperator:
         self.world, self.rank, self.part = int(world), int(rank), None
         if self.world > 1:
             # domain decomposition of the renumbered mesh (partition.py)
-            from ..partition import HaloExchange, build_partition, slab_owner
-            if mortars is not None and len(mortars):
-                raise NotImplementedError("partitioned AMR meshes are not supported yet")
+            from ..partition import (build_partition, local_mortars, mortar_aligned_owner,
+                                     slab_owner)
             owner = slab_owner(self.layout_mesh, self.world, period=period)
+            part_mortars = None
+            if mortars is not None and len(mortars):
+                # nonconforming interfaces stay rank-local: the fine halves
+                # of every hanging edge go to the coarse element's rank
+                owner = mortar_aligned_owner(self.layout_mesh, mortars, owner)
             self.part = build_partition(self.layout_mesh, lcol.colors, lcol.n_colors, owner,
                                         self.rank)
+            if mortars is not None and len(mortars):
+                part_mortars = local_mortars(self.part, mortars)
             self.surfaces = build_surface_list(self.part.mesh, self.part.colors, lcol.n_colors,
                                                period=period, owned=self.part.n_owned,
-                                               flipped=self.part.flipped, **self._sort)
+                                               flipped=self.part.flipped, mortars=part_mortars,
+                                               **self._sort)
             self.n_elements = self.part.n_owned
             self.n_local = self.part.n_local
         else:

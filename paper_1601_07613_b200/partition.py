@@ -43,6 +43,56 @@ def slab_owner(mesh: Mesh, world: int, axis: int | None = None, period=None) -> 
     return owner
 
 
+def mortar_aligned_owner(mesh: Mesh, mortars, owner: np.ndarray) -> np.ndarray:
+    """``owner`` with every hanging interface made rank-local.  The coarse
+    element of each (full, half_lo, half_hi) triple (left of ``full``) and
+    the fine elements of its halves (``layout.py`` mortar surfaces: fine
+    child left, coarse element right) are linked; each connected group
+    (a corner child can hang on two coarse neighbours, a level-2 child on a
+    level-1 one) moves to the rank that owns most of its elements (ties:
+    the lowest rank).  Mortar surfaces then never cross a cut; only
+    conforming surfaces carry ghosts."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+    mortars = np.asarray(mortars, dtype=np.int64).reshape(-1, 3)
+    owner = np.asarray(owner, dtype=np.int64).copy()
+    if not len(mortars):
+        return owner
+    L = mesh.surf_elems[:, 0]
+    coarse = L[mortars[:, 0]]
+    a = np.concatenate([coarse, coarse])
+    b = np.concatenate([L[mortars[:, 1]], L[mortars[:, 2]]])
+    ne = mesh.n_elements
+    g = coo_matrix((np.ones(len(a)), (a, b)), shape=(ne, ne))
+    _, comp = connected_components(g, directed=False)
+    linked = np.zeros(ne, dtype=bool)
+    linked[a] = linked[b] = True
+    ids = np.flatnonzero(linked)
+    world = int(owner.max()) + 1
+    votes = np.zeros((comp.max() + 1, world), dtype=np.int64)
+    np.add.at(votes, (comp[ids], owner[ids]), 1)
+    owner[ids] = votes.argmax(axis=1)[comp[ids]]
+    return owner
+
+
+def local_mortars(part: "Partition", mortars) -> np.ndarray:
+    """The hanging triples of ``part``'s owned coarse elements in its local
+    surface ids (all three surfaces are local after
+    ``mortar_aligned_owner``)."""
+    mortars = np.asarray(mortars, dtype=np.int64).reshape(-1, 3)
+    loc = np.full(int(max(part.global_surface.max(initial=-1), mortars.max(initial=-1))) + 1, -1,
+                  dtype=np.int64)
+    loc[part.global_surface] = np.arange(len(part.global_surface))
+    m = loc[mortars]
+    keep = (m >= 0).any(axis=1)
+    if not (m[keep] >= 0).all():
+        raise AssertionError("hanging interface split across ranks")
+    m = m[keep]
+    if (part.mesh.surf_elems[m[:, 0], 0] >= part.n_owned).any():
+        raise AssertionError("coarse element of a local hanging interface is a ghost")
+    return m
+
+
 @dataclass
 class Partition:
     rank: int

@@ -97,6 +97,56 @@ def test_local_layout_orders_ghost_surfaces_last(world):
         assert sweeps_oracle.first_race(se, col, lc.n_colors) is None
 
 
+def amr_layout_case(targets=(0, 5, 17, 18, 40, 77, 100), levels=1):
+    base = P.gen_tri_rect(10, 8)
+    col, _ = P.color(base)
+    ref, fine = P.refine(base, col, list(targets))
+    if levels == 2:
+        kids = np.flatnonzero(ref.child_slot < 0)[::9]
+        ref, fine = P.refine(ref, fine, kids.tolist())
+    mortars = ref.hanging_array()
+    plan = P.build_plan(ref.mesh, fine)
+    lm, lc = P.apply_plan(ref.mesh, fine, plan)
+    return lm, lc, plan.surface_perm[mortars]
+
+
+@pytest.mark.parametrize("world,levels", [(2, 1), (3, 1), (4, 2)])
+def test_partitioned_amr_keeps_hanging_interfaces_rank_local(world, levels):
+    """Partitioned AMR: the fine halves of every hanging edge follow the
+    coarse element's rank, so each rank's local layout carries whole mortar
+    triples; every local surface that touches no ghost has the same sides
+    and flags as in the single-domain layout."""
+    from paper_1601_07613_b200.dg.layout import FLAG_R_GHOST, build_surface_list
+    from paper_1601_07613_b200.partition import local_mortars, mortar_aligned_owner
+    lm, lc, mortars = amr_layout_case(levels=levels)
+    assert len(mortars)
+    owner = mortar_aligned_owner(lm, mortars, slab_owner(lm, world))
+    L = lm.surf_elems[:, 0]
+    for k in (1, 2):
+        assert np.array_equal(owner[L[mortars[:, k]]], owner[L[mortars[:, 0]]])
+    assert len(np.unique(owner)) == world
+    single = build_surface_list(lm, lc.colors, lc.n_colors, mortars=mortars)
+    ref = {int(ms): (int(a), int(b), int(c)) for ms, a, b, c in
+           zip(single.mesh_surface, single.left, single.right, single.code)}
+    n_triples = 0
+    for r in range(world):
+        part = build_partition(lm, lc.colors, lc.n_colors, owner, r)
+        lmort = local_mortars(part, mortars)
+        n_triples += len(lmort)
+        sl = build_surface_list(part.mesh, part.colors, lc.n_colors, owned=part.n_owned,
+                                flipped=part.flipped, mortars=lmort)
+        gids = np.concatenate([part.owned, part.ghosts])
+        for ms, a, b, c in zip(sl.mesh_surface, sl.left, sl.right, sl.code):
+            if c & FLAG_R_GHOST or part.flipped[ms]:
+                continue
+            g = int(part.global_surface[ms])
+            assert ref[g] == (int(gids[a]), int(gids[b]) if b >= 0 else -1, int(c))
+        se = np.stack([sl.left, sl.right], 1).astype(np.int64)
+        col = np.repeat(np.arange(1, lc.n_colors + 1), np.diff(sl.bounds))
+        assert sweeps_oracle.first_race(se, col, lc.n_colors) is None
+    assert n_triples == len(mortars)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

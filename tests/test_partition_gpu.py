@@ -143,3 +143,41 @@ def test_tet_slabs_with_kernel_packed_exchange(cuda, world, dims):
         rows = Ud[: op.n_elements, : op.block_width()].cpu().numpy()
         got[op.owned_user_ids()] = rows.reshape(op.n_elements, op.n_equations, op.n_basis)
     assert np.array_equal(got, want), np.abs(got - want).max()
+
+
+@pytest.mark.parametrize("world,levels", [(2, 1), (3, 2)])
+def test_partitioned_amr_matches_single_domain(cuda, world, levels):
+    """Partitioned nonconforming mesh (hanging interfaces kept rank-local by
+    ``mortar_aligned_owner``): owned results equal the single domain bit
+    for bit after two SSP-RK3 steps."""
+    import torch
+    base = P.gen_tri_rect(12, 10)
+    col, _ = P.color(base)
+    cen = base.vertices[base.elem_verts[:, :3]].mean(axis=1)
+    tg = np.flatnonzero(((cen - [6, 5]) ** 2).sum(1) < 10).tolist()
+    ref, fine = P.refine(base, col, tg)
+    if levels == 2:
+        kids = np.flatnonzero(ref.child_slot < 0)[::9]
+        ref, fine = P.refine(ref, fine, kids.tolist())
+    single = DGOperator(ref, fine, degree=2, physics="euler")
+    assert len(single.mortars)
+    U = single.initial_state("wave")
+    dt = single.stable_dt(0.2)
+    want = single.ssprk3(U, dt, 2)
+    ops = [DGOperator(ref, fine, degree=2, physics="euler", world=world, rank=r)
+           for r in range(world)]
+    assert sum(len(op.surfaces.left) for op in ops) > len(single.surfaces.left)
+    Us = [torch.from_numpy(op.to_internal(U)).cuda() for op in ops]
+    works = [op.work_device() for op in ops]
+    for _ in range(2):
+        for mode, a, b in DGOperator.STAGES:
+            emulated_exchange(ops, Us)
+            for op, Ud, w in zip(ops, Us, works):
+                for c in range(1, op.n_colors + 1):
+                    op.color_pass_device(c, Ud, w[0], w[1], mode, a, b, dt)
+    torch.cuda.synchronize()
+    got = np.empty_like(want)
+    for op, Ud in zip(ops, Us):
+        rows = Ud[: op.n_elements, : op.block_width()].cpu().numpy()
+        got[op.owned_user_ids()] = rows.reshape(op.n_elements, op.n_equations, op.n_basis)
+    assert np.array_equal(got, want), np.abs(got - want).max()
