@@ -142,6 +142,11 @@ int mc_default_payload_dev(int64_t n, int64_t seed, int64_t* out_dev,
 #define MC_KIND_TRI 0
 #define MC_KIND_QUAD 1
 #define MC_KIND_TET 2
+/* conforming triangle + quadrilateral mix (2D); element blocks have the
+ * quad basis size, triangles use its first (p+1)(p+2)/2 modes per equation
+ * (the rest stay zero); face codes 0-23 quad sides, 24-41 triangle sides;
+ * volume tables: the quad rule's rows, then the triangle rule's */
+#define MC_KIND_HYBRID 3
 #define MC_PHYS_ADVECTION 0
 #define MC_PHYS_EULER 1
 
@@ -194,6 +199,8 @@ typedef struct mc_dg_desc {
    * 1e-5 tolerance).  Every U / U0 / R / work / send-buffer pointer of an
    * fp32 operator points to floats, strides count floats. */
   int state_f32;
+  /* MC_KIND_HYBRID: per element (ne+ng) 0 = triangle, 1 = quad; else NULL */
+  const uint8_t* elem_kind;
 } mc_dg_desc;
 
 typedef struct mc_dg mc_dg;

@@ -36,8 +36,12 @@ import numpy as np
 
 SIDES = {"tri": ((0, 1), (1, 2), (2, 0)), "quad": ((0, 1), (1, 2), (2, 3), (3, 0)),
          "tet": ((0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3))}
-NVERT = {"tri": 3, "quad": 4, "tet": 4}
-DIMS = {"tri": 2, "quad": 2, "tet": 3}
+NVERT = {"tri": 3, "quad": 4, "tet": 4, "hybrid": 4}
+DIMS = {"tri": 2, "quad": 2, "tet": 3, "hybrid": 2}
+# "hybrid": a conforming triangle + quad mix (Problem.elem_kind 0 / 1); each
+# element uses its own kind's basis and rules, coefficient arrays are
+# quad-sized and a triangle's modes beyond its N_p stay zero
+HYB_KINDS = ((0, "tri"), (1, "quad"))
 
 
 # ----------------------------------------------------------- quadrature
@@ -261,10 +265,14 @@ class Problem:
     active: np.ndarray          # surfaces taking part (full coarse edges off)
     period: tuple | None = None
     cache: dict = field(default_factory=dict)
+    elem_kind: np.ndarray | None = None   # "hybrid": 0 triangle, 1 quad
 
 
 def element_coords(prob: Problem):
-    X = prob.vertices[prob.elem_verts[:, :NVERT[prob.kind]]].copy()
+    ev = prob.elem_verts[:, :NVERT[prob.kind]]
+    if prob.kind == "hybrid":               # a triangle's 4th slot: its 3rd vertex
+        ev = np.where(ev >= 0, ev, ev[:, 2:3])
+    X = prob.vertices[ev].copy()
     if prob.period is not None:
         for d, L in enumerate(prob.period):
             if L:
@@ -290,18 +298,58 @@ def _to_ref(Jinv, x0, x, period, centre):
     return np.einsum("nrd,ngd->ngr", Jinv, x - x0[:, None, :])
 
 
+def _setup_hybrid(prob: Problem, c: dict, X):
+    """Per-kind geometry, bases and volume rules of a hybrid mesh."""
+    ek = np.asarray(prob.elem_kind)
+    ne = len(X)
+    det = np.empty(ne)
+    Jinv = np.empty((ne, 2, 2))
+    centre = np.empty((ne, 2))
+    parts = {}
+    for code, kind in HYB_KINDS:
+        idx = np.flatnonzero(ek == code)
+        B = Basis(kind, prob.p)
+        vP, vW = vol_rule(kind, prob.p)
+        if len(idx):
+            _, det[idx], Jinv[idx] = _affine(kind, X[idx][:, :NVERT[kind]])
+            centre[idx] = X[idx][:, :NVERT[kind]].mean(axis=1)
+        parts[code] = dict(idx=idx, B=B, vW=vW, vphi=B.values(vP), vdphi=B.gradients(vP))
+    nb = parts[1]["B"].scale.size
+    c.update(X=X, det=det, Jinv=Jinv, centre=centre, parts=parts, nb=nb, ek=ek)
+
+
+def _values_padded(c: dict, prob: Problem, elems, xi):
+    """Basis values at reference points xi (s, g, dim) of elements, each on
+    its own kind's basis, padded to the coefficient width."""
+    if prob.kind != "hybrid":
+        return c["B"].values(xi.reshape(-1, xi.shape[-1])).reshape(xi.shape[0], xi.shape[1], -1)
+    out = np.zeros(xi.shape[:2] + (c["nb"],))
+    for code, _ in HYB_KINDS:
+        m = c["ek"][elems] == code
+        if m.any():
+            B = c["parts"][code]["B"]
+            v = B.values(xi[m].reshape(-1, xi.shape[-1])).reshape(int(m.sum()), xi.shape[1], -1)
+            out[m, :, :v.shape[-1]] = v
+    return out
+
+
 def setup(prob: Problem):
     c = prob.cache
     if c:
         return c
     kind, p = prob.kind, prob.p
-    B = Basis(kind, p)
     X = element_coords(prob)
-    J, det, Jinv = _affine(kind, X)
-    vP, vW = vol_rule(kind, p)
-    fP, fW = surf_rule(kind, p)
-    c.update(B=B, X=X, det=det, Jinv=Jinv, vW=vW, fW=fW, vphi=B.values(vP),
-             vdphi=B.gradients(vP), centre=X.mean(axis=1))
+    fP, fW = surf_rule("tri" if kind == "hybrid" else kind, p)
+    if kind == "hybrid":
+        _setup_hybrid(prob, c, X)
+        c.update(fW=fW)
+    else:
+        B = Basis(kind, p)
+        J, det, Jinv = _affine(kind, X)
+        vP, vW = vol_rule(kind, p)
+        c.update(B=B, X=X, det=det, Jinv=Jinv, vW=vW, fW=fW, vphi=B.values(vP),
+                 vdphi=B.gradients(vP), centre=X.mean(axis=1))
+    det, Jinv = c["det"], c["Jinv"]
     # per surface: physical quadrature points in the left element's frame
     sid = np.flatnonzero(prob.active)
     L = prob.surf_elems[sid, 0]
@@ -328,13 +376,13 @@ def setup(prob: Problem):
     out = ((corners.mean(axis=1) - c["centre"][L]) * nrm).sum(1) < 0
     nrm[out] *= -1
     xiL = _to_ref(Jinv[L], X[L, 0], xg, prob.period, c["centre"][L])
-    phiL = B.values(xiL.reshape(-1, xiL.shape[-1])).reshape(len(sid), len(fW), -1)
+    phiL = _values_padded(c, prob, L, xiL)
     inner = R >= 0
     phiR = np.zeros_like(phiL)
     if inner.any():
         xiR = _to_ref(Jinv[R[inner]], X[R[inner], 0], xg[inner], prob.period,
                       c["centre"][R[inner]])
-        phiR[inner] = B.values(xiR.reshape(-1, xiR.shape[-1])).reshape(inner.sum(), len(fW), -1)
+        phiR[inner] = _values_padded(c, prob, R[inner], xiR)
     c.update(sid=sid, L=L, R=R, n=nrm, meas=meas, phiL=phiL, phiR=phiR,
              col=prob.colors[sid])
     return c
@@ -346,6 +394,19 @@ def volume_term(prob: Problem, U: np.ndarray, lo: int = 0, hi: int | None = None
     the elements [lo, hi) only (U still indexed globally)."""
     c = setup(prob)
     hi = len(U) if hi is None else hi
+    if prob.kind == "hybrid":
+        out = np.zeros((hi - lo,) + U.shape[1:])
+        for code, _ in HYB_KINDS:
+            pt = c["parts"][code]
+            idx = pt["idx"][(pt["idx"] >= lo) & (pt["idx"] < hi)]
+            if not len(idx):
+                continue
+            nk = pt["vphi"].shape[1]
+            Uq = np.einsum("qj,ekj->eqk", pt["vphi"], U[idx][:, :, :nk])
+            Ft = np.einsum("erd,eqdk->eqrk", c["Jinv"][idx], prob.physics.flux(Uq))
+            out[idx - lo, :, :nk] = np.einsum("q,rqj,eqrk->ekj", pt["vW"], pt["vdphi"], Ft,
+                                              optimize=True)
+        return out
     Uq = np.einsum("qj,ekj->eqk", c["vphi"], U[lo:hi])
     F = prob.physics.flux(Uq)                                  # (e, q, d, k)
     Ft = np.einsum("erd,eqdk->eqrk", c["Jinv"][lo:hi], F)      # contravariant
@@ -413,6 +474,19 @@ def ssprk3(prob: Problem, U: np.ndarray, dt: float, steps: int = 1) -> np.ndarra
 def project(prob: Problem, fn) -> np.ndarray:
     """L2 projection of fn(x (n, d)) -> (n, neq) onto the basis."""
     c = setup(prob)
+    if prob.kind == "hybrid":
+        out = None
+        for code, kind in HYB_KINDS:
+            idx = c["parts"][code]["idx"]
+            vP, vW = vol_rule(kind, prob.p + 1)
+            phi = c["parts"][code]["B"].values(vP)
+            x = c["X"][idx, 0][:, None, :] + np.einsum("erd,qd->eqr",
+                                                        np.linalg.inv(c["Jinv"][idx]), vP)
+            vals = fn(x.reshape(-1, x.shape[-1])).reshape(x.shape[0], x.shape[1], -1)
+            if out is None:
+                out = np.zeros((len(c["X"]), vals.shape[-1], c["nb"]))
+            out[idx, :, :phi.shape[1]] = np.einsum("q,qj,eqk->ekj", vW, phi, vals)
+        return out
     vP, vW = vol_rule(prob.kind, prob.p + 1)
     phi = c["B"].values(vP)
     x = c["X"][:, 0][:, None, :] + np.einsum("erd,qd->eqr",
@@ -424,6 +498,13 @@ def project(prob: Problem, fn) -> np.ndarray:
 def mass_weights(prob: Problem) -> np.ndarray:
     """|det J_e| * integral(phi_0): element mass of mode-0 coefficient."""
     c = setup(prob)
+    if prob.kind == "hybrid":
+        w = np.empty(len(c["X"]))
+        for code, kind in HYB_KINDS:
+            vP, vW = vol_rule(kind, prob.p + 1)
+            idx = c["parts"][code]["idx"]
+            w[idx] = np.abs(c["det"][idx]) * np.sum(vW * c["parts"][code]["B"].values(vP)[:, 0])
+        return w
     vP, vW = vol_rule(prob.kind, prob.p + 1)
     phi0 = c["B"].values(vP)[:, 0]
     return np.abs(c["det"]) * np.sum(vW * phi0)
@@ -435,7 +516,8 @@ def problem_from(desc: dict) -> Problem:
                    velocity=tuple(desc["velocity"]), farfield=tuple(desc["farfield"]))
     return Problem(desc["kind"], desc["p"], phys, desc["vertices"], desc["elem_verts"],
                    desc["surf_verts"], desc["surf_elems"], desc["colors"],
-                   desc["n_colors"], desc["active"], desc["period"])
+                   desc["n_colors"], desc["active"], desc["period"],
+                   elem_kind=desc.get("elem_kind"))
 
 
 def term_scale(prob: Problem, U: np.ndarray) -> float:

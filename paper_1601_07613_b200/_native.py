@@ -62,6 +62,7 @@ class DGDesc(C.Structure):
         ("gamma", C.c_double), ("velocity", C.c_double * 3),
         ("farfield", C.c_double * 5),
         ("state_f32", C.c_int),
+        ("elem_kind", C.c_void_p),
     ]
 
 

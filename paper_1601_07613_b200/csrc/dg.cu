@@ -25,6 +25,7 @@ struct mc_dg {
   // device allocations
   int32_t *d_left = nullptr, *d_right = nullptr, *d_slots = nullptr;
   uint32_t* d_code = nullptr;
+  uint8_t* d_ekind = nullptr;      // MC_KIND_HYBRID: element kinds (0 tri, 1 quad)
   double *d_geom = nullptr, *d_jinv = nullptr, *d_tables = nullptr, *d_ptables = nullptr;
   int64_t* d_slot_ptr = nullptr;
   double* d_buffer = nullptr;      // 2*ns blocks (buffered strategy)
@@ -218,6 +219,7 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   if (d->kind == MC_KIND_TRI) ops = mcdg::ops_tri(d->physics, d->degree);
   else if (d->kind == MC_KIND_QUAD) ops = mcdg::ops_quad(d->physics, d->degree);
   else if (d->kind == MC_KIND_TET) ops = mcdg::ops_tet(d->physics, d->degree);
+  else if (d->kind == MC_KIND_HYBRID) ops = mcdg::ops_hyb(d->physics, d->degree);
   if (!ops)
     return mc_fail(MC_EUNSUPPORTED, "no sm_100a kernel compiled for kind " +
                                         std::to_string(d->kind) + " physics " +
@@ -230,6 +232,12 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
     return mc_fail(MC_EUNSUPPORTED, "fp32 state needs the register kernels (N_eq * N_p <= 64)");
   if (d->n_elements <= 0 || d->n_surfaces < 0 || d->n_colors < 1 || d->n_ghosts < 0)
     return mc_fail(MC_EINVAL, "bad DG sizes");
+  if (d->kind == MC_KIND_HYBRID) {
+    if (!d->elem_kind) return mc_fail(MC_EINVAL, "hybrid mesh without element kinds");
+    for (int64_t i = 0; i < d->n_elements + d->n_ghosts; ++i)
+      if (d->elem_kind[i] > 1)
+        return mc_fail(MC_EINVAL, "element " + std::to_string(i) + " kind must be 0 or 1");
+  }
   if (d->n_elements + d->n_ghosts >= (int64_t(1) << 31) || d->n_surfaces >= (int64_t(1) << 31))
     return mc_fail(MC_EINVAL, "mesh too large for 32-bit ids");
   if (d->group_bounds[0] != 0 || d->group_bounds[d->n_colors] != d->n_surfaces)
@@ -301,6 +309,7 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   if (e == cudaSuccess) e = upload(&h->d_code, d->surf_code, h->ns);
   if (e == cudaSuccess) e = upload(&h->d_geom, d->surf_geom, h->ns * (dim + 2));
   if (e == cudaSuccess) e = upload(&h->d_jinv, d->elem_jinv, nall * dim * dim);
+  if (e == cudaSuccess && d->kind == MC_KIND_HYBRID) e = upload(&h->d_ekind, d->elem_kind, nall);
   if (e == cudaSuccess) e = upload(&h->d_tables, tables.data(), int64_t(tables.size()));
   if (e == cudaSuccess && d->elem_slot_ptr) e = upload(&h->d_slot_ptr, d->elem_slot_ptr, h->ne + 1);
   if (e == cudaSuccess && d->elem_slots)
@@ -324,6 +333,7 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   v.code = h->d_code;
   v.geom = h->d_geom;
   v.jinv = h->d_jinv;
+  v.ekind = h->d_ekind;
   v.tables = h->d_tables;
   v.slot_ptr = h->d_slot_ptr;
   v.slots = h->d_slots;
@@ -344,6 +354,7 @@ MC_API int mc_dg_destroy(mc_dg* h) {
   cudaFree(h->d_code);
   cudaFree(h->d_geom);
   cudaFree(h->d_jinv);
+  cudaFree(h->d_ekind);
   cudaFree(h->d_tables);
   cudaFree(h->d_ptables);
   cudaFree(h->d_slot_ptr);

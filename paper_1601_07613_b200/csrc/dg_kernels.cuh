@@ -37,7 +37,10 @@ namespace mcdg {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-enum Kind { TRI = 0, QUAD = 1, TET = 2 };
+// HYB: conforming triangle + quad mix; quad-sized blocks (triangles use the
+// first (p+1)(p+2)/2 modes of each equation), 24 quad + 18 triangle face
+// codes, the volume tables hold the quad rule's rows then the triangle's
+enum Kind { TRI = 0, QUAD = 1, TET = 2, HYB = 3 };
 enum Phys { ADV = 0, EULER = 1 };
 
 template <int K, int PH, int P>
@@ -46,13 +49,17 @@ struct Cfg {
   static constexpr int DIM = (K == TET) ? 3 : 2;
   static constexpr int NEQ = (PH == ADV) ? 1 : DIM + 2;
   static constexpr int NP = (K == TRI) ? (P + 1) * (P + 2) / 2
-                          : (K == QUAD) ? (P + 1) * (P + 1)
-                                        : (P + 1) * (P + 2) * (P + 3) / 6;
+                          : (K == QUAD || K == HYB) ? (P + 1) * (P + 1)
+                                                    : (P + 1) * (P + 2) * (P + 3) / 6;
   // quadrature (dg/basis.py): degree-5 symmetric rules for p = 2 on simplices
   static constexpr int NQF = (K == TET) ? (P == 2 ? 7 : (P + 1) * (P + 1)) : P + 1;
+  static constexpr int NQV_TRI = (P == 2) ? 7 : (P + 1) * (P + 1);
+  static constexpr int NQV_QUAD = (P + 1) * (P + 1);   // HYB: quad rows [0, NQV_QUAD)
   static constexpr int NQV = (K == TET) ? (P == 2 ? 14 : (P + 1) * (P + 1) * (P + 1))
-                           : (K == TRI && P == 2) ? 7 : (P + 1) * (P + 1);
-  static constexpr int NCODES = (K == QUAD || K == TET) ? 24 : 18;
+                           : (K == TRI) ? NQV_TRI
+                           : (K == HYB) ? NQV_QUAD + NQV_TRI : NQV_QUAD;
+  static constexpr int NCODES = (K == QUAD || K == TET) ? 24 : (K == HYB) ? 42 : 18;
+  static constexpr int TRI_CODE0 = 24;                  // HYB: first triangle face code
 #ifdef MC_DG_DMMA
   static constexpr bool DMMA_ON = (K != TET);
 #else
@@ -86,12 +93,12 @@ struct Cfg {
   // Tables (computed at operator creation from vol_phi / vol_dphi):
   // WPSI[q][m] = w_q phi_m(q), DMAT[r][j][m]; modes are ordered by total
   // degree, so D_r[j][m] = 0 unless m < NPL(deg(j) - 1).
-  static constexpr int NPL = (K == QUAD || NEQ * NP > 64) ? 1
+  static constexpr int NPL = (K == QUAD || K == HYB || NEQ * NP > 64) ? 1
                            : (K == TRI) ? P * (P + 1) / 2 : P * (P + 1) * (P + 2) / 6;
 #ifdef MC_NO_P1PROJ
   static constexpr bool P1PROJ = false;
 #else
-  static constexpr bool P1PROJ = (K != QUAD) && P >= 1 && NEQ * NP <= 64;
+  static constexpr bool P1PROJ = (K != QUAD && K != HYB) && P >= 1 && NEQ * NP <= 64;
 #endif
   static constexpr int T_WPSI = T_VW + NQV;
   static constexpr int T_DMAT = T_WPSI + NQV * NPL;
@@ -213,6 +220,7 @@ struct View {
   int64_t n_surfaces;
   int64_t stride;      // doubles per element block
   Params prm;
+  const uint8_t* ekind;     // HYB: per element 0 = triangle, 1 = quad
   // partitioned runs: the last-touch pass of an RK stage also writes each
   // interface element's new block into its slot of the ghost-exchange send
   // buffer (send_slot[e] >= 0), so the next stage posts it without a pack

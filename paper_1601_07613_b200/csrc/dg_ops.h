@@ -40,6 +40,7 @@ struct Ops {
 Ops* ops_tri(int phys, int p);
 Ops* ops_quad(int phys, int p);
 Ops* ops_tet(int phys, int p);
+Ops* ops_hyb(int phys, int p);
 
 // Instantiation helper used by the per-kind translation units.
 template <int K, int PH, int P>

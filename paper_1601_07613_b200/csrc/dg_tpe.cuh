@@ -353,7 +353,7 @@ template <class C, int PH>
 __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[Tpe<C>::WH],
                                            const double* __restrict__ jinv_e, int h, int nown,
                                            bool mine, const Params& P,
-                                           double (&acc)[Tpe<C>::WH]) {
+                                           double (&acc)[Tpe<C>::WH], int ek = 0) {
   constexpr int WH = Tpe<C>::WH, NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH, DIM = C::DIM;
   const double* vphi = vol_tables<C, true>(st);
   const double* vdphi = vphi + (C::S_VDPHI - C::S_VPHI);
@@ -432,8 +432,11 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   }
 #endif
   constexpr int kUnroll = kVolUnroll<Tpe<C>::H>;
+  // volume points [qa, qb) of the tables; `on` = this lane's element uses
+  // them (HYB: the quad rule's rows, then the triangle rule's)
+  auto points = [&](int qa, int qb, bool on) {
 #pragma unroll kUnroll
-  for (int q = 0; q < C::NQV; ++q) {
+  for (int q = qa; q < qb; ++q) {
     double own[NEQH], s[NEQ];
 #pragma unroll
     for (int k = 0; k < NEQH; ++k) own[k] = tdot<NP, WH>(vphi + q * C::NPP, u, k * NP);
@@ -471,13 +474,28 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
         for (int k = 0; k < NEQH; ++k) {
           // uniform control flow (zero factor for idle lanes) keeps the
           // constant-memory table reads warp-uniform (c3: 0.94 -> 0.97)
-          const double f = (mine && k < nown) ? w * own_part<C>(Ft + r * NEQ, h, k) : 0.0;
+          const double f = (mine && on && k < nown) ? w * own_part<C>(Ft + r * NEQ, h, k) : 0.0;
           taxpy<NP, WH>(dp, f, acc, k * NP);
         }
       }
     }
   }
+  };
+  if constexpr (C::KIND == HYB) {
+    // conforming triangle + quad mix: each element integrates with its own
+    // kind's rule and basis (triangle rows are zero beyond its N_p)
+    if constexpr (Tpe<C>::H == 1) {   // called per lane (no shuffles)
+      if (ek) points(0, C::NQV_QUAD, true);
+      else points(C::NQV_QUAD, C::NQV, true);
+    } else {                          // the whole warp takes part (shuffles)
+      if (__any_sync(kFull, mine && ek)) points(0, C::NQV_QUAD, ek != 0);
+      if (__any_sync(kFull, mine && !ek)) points(C::NQV_QUAD, C::NQV, ek == 0);
+    }
+  } else {
+    points(0, C::NQV, true);
+  }
 }
+
 
 struct TpeSide {
   int e, mycode;
@@ -1017,6 +1035,41 @@ __device__ __forceinline__ void fstore(float* dst, int n, const double (&src)[N]
     if (kWhole || j < n) dst[j] = __double2float_rn(src[j]);
 }
 
+// fp32 runs that are only 8-byte aligned (two lanes per side with an odd
+// basis size, e.g. quads / hybrid meshes at p = 2: lane 1 starts 18 floats
+// into the block): 64-bit float pairs instead of 128-bit quads
+template <int N, bool kWhole>
+__device__ __forceinline__ void fload2(const float* src, int n, double (&dst)[N], bool nc) {
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j) {
+    if (kWhole || 2 * j + 2 <= n) {
+      float x, y;
+      if (nc)
+        asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(x), "=f"(y)
+            : "l"(src + 2 * j));
+      else
+        asm("ld.global.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(x), "=f"(y)
+            : "l"(src + 2 * j));
+      dst[2 * j] = x;
+      dst[2 * j + 1] = y;
+    } else {
+      dst[2 * j] = dst[2 * j + 1] = 0.0;
+    }
+  }
+  if constexpr (N % 2) dst[N - 1] = (kWhole || N <= n) ? double(src[N - 1]) : 0.0;
+}
+
+template <int N, bool kWhole>
+__device__ __forceinline__ void fstore2(float* dst, int n, const double (&src)[N]) {
+#pragma unroll
+  for (int j = 0; j < N / 2; ++j)
+    if (kWhole || 2 * j + 2 <= n)
+      *reinterpret_cast<float2*>(dst + 2 * j) =
+          make_float2(__double2float_rn(src[2 * j]), __double2float_rn(src[2 * j + 1]));
+  if constexpr (N % 2)
+    if (kWhole || N <= n) dst[N - 1] = __double2float_rn(src[N - 1]);
+}
+
 // state-type dispatch: S = double (the default) or float
 template <int N, bool kWhole, bool kV4>
 __device__ __forceinline__ void sload(const double* src, int n, double (&dst)[N]) {
@@ -1024,7 +1077,8 @@ __device__ __forceinline__ void sload(const double* src, int n, double (&dst)[N]
 }
 template <int N, bool kWhole, bool kV4>
 __device__ __forceinline__ void sload(const float* src, int n, double (&dst)[N]) {
-  fload<N, kWhole>(src, n, dst, true);
+  if constexpr (kWhole || kV4) fload<N, kWhole>(src, n, dst, true);
+  else fload2<N, kWhole>(src, n, dst, true);
 }
 template <int N, bool kWhole, bool kV4>
 __device__ __forceinline__ void sload_rw(const double* src, int n, double (&dst)[N]) {
@@ -1032,7 +1086,8 @@ __device__ __forceinline__ void sload_rw(const double* src, int n, double (&dst)
 }
 template <int N, bool kWhole, bool kV4>
 __device__ __forceinline__ void sload_rw(const float* src, int n, double (&dst)[N]) {
-  fload<N, kWhole>(src, n, dst, false);
+  if constexpr (kWhole || kV4) fload<N, kWhole>(src, n, dst, false);
+  else fload2<N, kWhole>(src, n, dst, false);
 }
 template <int N, bool kWhole, bool kV4>
 __device__ __forceinline__ void sstore(double* dst, int n, const double (&src)[N]) {
@@ -1040,7 +1095,8 @@ __device__ __forceinline__ void sstore(double* dst, int n, const double (&src)[N
 }
 template <int N, bool kWhole, bool kV4>
 __device__ __forceinline__ void sstore(float* dst, int n, const double (&src)[N]) {
-  fstore<N, kWhole>(dst, n, src);
+  if constexpr (kWhole || kV4) fstore<N, kWhole>(dst, n, src);
+  else fstore2<N, kWhole>(dst, n, src);
 }
 
 template <class C>
@@ -1186,10 +1242,12 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
     }
     if constexpr (kVol) {
       const double* jp = v.jinv + int64_t(first ? t.e : 0) * (C::DIM * C::DIM);
+      int ek = 0;
+      if constexpr (C::KIND == HYB) ek = first ? __ldg(v.ekind + t.e) : 0;
       if constexpr (T::H == 1) {
-        if (first) tpe_volume<C, PH>(st, u, jp, 0, ln.nown, true, v.prm, acc);
+        if (first) tpe_volume<C, PH>(st, u, jp, 0, ln.nown, true, v.prm, acc, ek);
       } else if (__any_sync(kFull, first)) {   // the whole warp takes part in the shuffles
-        tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc);
+        tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc, ek);
       }
       if (t.owner && !first) sload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     }
@@ -1294,8 +1352,10 @@ k_tpe_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
     }
 #pragma unroll
     for (int j = 0; j < WH; ++j) acc[j] = 0.0;
+    int ek = 0;
+    if constexpr (C::KIND == HYB) ek = has ? __ldg(v.ekind + e) : 0;
     tpe_volume<C, PH>(st, u, v.jinv + (has ? e : 0) * (C::DIM * C::DIM), h, nown, has, v.prm,
-                      acc);
+                      acc, ek);
     if (has) tstore<WH, kWhole, T::V4>(R + off, n, acc);
   }
 }

@@ -16,4 +16,4 @@ int mc_fail(int code, const std::string& msg) {
 
 extern "C" MC_API const char* mc_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" MC_API int mc_abi_version(void) { return 1010; }
+extern "C" MC_API int mc_abi_version(void) { return 1011; }  // 1011: mc_dg_desc.elem_kind (hybrid meshes)

@@ -55,11 +55,33 @@ EDGE_VARIANTS = ((0.0, 1.0), (1.0, 0.0), (0.0, 0.5), (0.5, 0.0),
 FACE_PERMS = tuple(itertools.permutations(range(3)))
 
 
-def n_face_codes(kind: ElementKind) -> int:
+class _HybridKind:
+    """The DG element kind of a conforming triangle + quad mix (the
+    reference's hybrid meshes, ``coloring.py:38-42``): quad-sized blocks,
+    triangles on their first (p+1)(p+2)/2 modes."""
+    value = "hybrid"
+    name = "HYBRID"
+    n_vertices = 4
+
+    def __repr__(self):
+        return "HYBRID"
+
+
+HYBRID = _HybridKind()
+DIM[HYBRID] = 2
+# face codes of a hybrid layout: quad sides 0..23, triangle sides from here
+HYBRID_TRI_CODE0 = 24
+
+
+def n_face_codes(kind) -> int:
+    if kind is HYBRID:
+        return HYBRID_TRI_CODE0 + len(SIDE_POSITIONS[ElementKind.TRIANGLE]) * 6
     return len(SIDE_POSITIONS[kind]) * 6
 
 
-def basis_size(kind: ElementKind, p: int) -> int:
+def basis_size(kind, p: int) -> int:
+    if kind is HYBRID:
+        kind = ElementKind.QUAD
     if kind is ElementKind.TRIANGLE:
         return (p + 1) * (p + 2) // 2
     if kind is ElementKind.QUAD:
@@ -311,9 +333,36 @@ class ReferenceTables:
 _TABLE_CACHE: dict = {}
 
 
-def reference_tables(kind: ElementKind, p: int) -> ReferenceTables:
+def _hybrid_tables(p: int) -> ReferenceTables:
+    """Quad and triangle tables in one layout (``MC_KIND_HYBRID``): face
+    codes = the quad's 24 then the triangle's 18, volume rows = the quad
+    rule's then the triangle rule's; triangle rows are zero beyond its
+    basis size.  Both kinds share the edge rule."""
+    q = reference_tables(ElementKind.QUAD, p)
+    t = reference_tables(ElementKind.TRIANGLE, p)
+    nb = q.n_basis
+
+    def pad(a):
+        out = np.zeros(a.shape[:-1] + (nb,))
+        out[..., :a.shape[-1]] = a
+        return out
+
+    assert np.array_equal(q.face_w, t.face_w)
+    face_phi = np.concatenate([q.face_phi, pad(t.face_phi)], axis=0)
+    vol_phi = np.concatenate([q.vol_phi, pad(t.vol_phi)], axis=0)
+    vol_dphi = np.concatenate([q.vol_dphi, pad(t.vol_dphi)], axis=1)
+    vol_w = np.concatenate([q.vol_w, t.vol_w])
+    vol_pts = np.concatenate([q.vol_pts, t.vol_pts])
+    return ReferenceTables(HYBRID, p, nb, face_phi.shape[0], q.face_w, face_phi, vol_w,
+                           vol_phi, vol_dphi, vol_pts, q.face_pts)
+
+
+def reference_tables(kind, p: int) -> ReferenceTables:
     key = (kind, p)
     if key in _TABLE_CACHE:
+        return _TABLE_CACHE[key]
+    if kind is HYBRID:
+        _TABLE_CACHE[key] = _hybrid_tables(p)
         return _TABLE_CACHE[key]
     nb = basis_size(kind, p)
     vpts, vw = volume_rule(kind, p)

@@ -37,7 +37,7 @@ import numpy as np
 
 from ..errors import WriteConflictError
 from ..mesh import ElementKind, Mesh, SIDE_POSITIONS, CODE_TO_KIND
-from .basis import DIM, EDGE_VARIANTS, FACE_PERMS
+from .basis import DIM, EDGE_VARIANTS, FACE_PERMS, HYBRID, HYBRID_TRI_CODE0
 
 FLAG_L_FIRST = 1 << 12
 FLAG_L_LAST = 1 << 13
@@ -47,19 +47,33 @@ FLAG_R_GHOST = 1 << 16
 FLAG_FLIPPED = 1 << 17
 
 
-def mesh_kind(mesh: Mesh) -> ElementKind:
+def mesh_kind(mesh: Mesh):
+    """The DG element kind: a single ElementKind, or ``HYBRID`` for a
+    conforming triangle + quad mix."""
     kinds = mesh.element_kind_profile
+    if kinds == {ElementKind.TRIANGLE, ElementKind.QUAD}:
+        return HYBRID
     if len(kinds) != 1:
-        raise NotImplementedError("DG operator needs a single-kind mesh")
+        raise NotImplementedError("DG operator needs a single-kind or a triangle + quad mesh")
     return next(iter(kinds))
+
+
+def element_kinds(mesh: Mesh) -> np.ndarray:
+    """(ne,) uint8 element kind codes (0 triangle, 1 quad, 2 tet)."""
+    return np.asarray(mesh.elem_kind, dtype=np.uint8)
 
 
 def unwrapped_element_coords(mesh: Mesh, period=None) -> np.ndarray:
     """(ne, nvert, dim) vertex coordinates per element; periodic generator
-    meshes are unwrapped relative to local vertex 0."""
+    meshes are unwrapped relative to local vertex 0.  Hybrid meshes: 4
+    slots, a triangle's fourth repeats its third vertex (``element_centroids``
+    averages the real ones)."""
     kind = mesh_kind(mesh)
     nvert = kind.n_vertices
-    X = mesh.vertices[mesh.elem_verts[:, :nvert]].copy()
+    ev = mesh.elem_verts[:, :nvert]
+    if kind is HYBRID:
+        ev = np.where(ev >= 0, ev, ev[:, 2:3])
+    X = mesh.vertices[ev].copy()
     if period is not None:
         for d, L in enumerate(period):
             if not L:
@@ -69,8 +83,26 @@ def unwrapped_element_coords(mesh: Mesh, period=None) -> np.ndarray:
     return X
 
 
-def element_geometry(kind: ElementKind, X: np.ndarray):
-    """Affine map x = x0 + J xi per element: (detJ (ne,), Jinv (ne,d,d))."""
+def element_centroids(mesh: Mesh, X: np.ndarray) -> np.ndarray:
+    """Vertex centroids from ``unwrapped_element_coords`` output."""
+    if mesh_kind(mesh) is not HYBRID:
+        return X.mean(axis=1)
+    quad = element_kinds(mesh) == 1
+    S = X[:, :3].sum(axis=1) + np.where(quad, 1.0, 0.0)[:, None] * X[:, 3]
+    return S / np.where(quad, 4.0, 3.0)[:, None]
+
+
+def element_geometry(kind, X: np.ndarray, ekind=None):
+    """Affine map x = x0 + J xi per element: (detJ (ne,), Jinv (ne,d,d)).
+    Hybrid: ``ekind`` (0 triangle, 1 quad) picks each element's map."""
+    if kind is HYBRID:
+        det = np.empty(len(X))
+        inv = np.empty((len(X), 2, 2))
+        for code, k in ((0, ElementKind.TRIANGLE), (1, ElementKind.QUAD)):
+            m = ekind == code
+            if m.any():
+                det[m], inv[m] = element_geometry(k, X[m][:, :k.n_vertices])
+        return det, inv
     if kind is ElementKind.QUAD:
         J = np.stack([X[:, 1] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)
         skew = X[:, 2] - (X[:, 1] + X[:, 3] - X[:, 0])
@@ -119,6 +151,20 @@ def _side_codes_2d(kind, elem_verts, elems, local, surf_verts, mids=None):
     return local * 6 + v
 
 
+def _side_codes_any(kind, ekind, elem_verts, elems, local, surf_verts, mids=None):
+    """2D side codes; hybrid meshes per element kind, triangle codes after
+    the quad's 24 (``HYBRID_TRI_CODE0``)."""
+    if kind is not HYBRID:
+        return _side_codes_2d(kind, elem_verts, elems, local, surf_verts, mids)
+    out = np.zeros(len(elems), dtype=np.int64)
+    for code, k, off in ((0, ElementKind.TRIANGLE, HYBRID_TRI_CODE0), (1, ElementKind.QUAD, 0)):
+        m = ekind[elems] == code
+        if m.any():
+            out[m] = off + _side_codes_2d(k, elem_verts, elems[m], local[m], surf_verts[m],
+                                          None if mids is None else mids[m])
+    return out
+
+
 def _side_codes_tet(elem_verts, elems, local, surf_verts):
     sides = np.asarray(SIDE_POSITIONS[ElementKind.TET])
     loc = sides[local]                                  # (n, 3) local vertex ids
@@ -156,6 +202,7 @@ class SurfaceList:
     slot_ptr: np.ndarray      # (ne+1,) CSR of (2*s+side) slots per element
     slots: np.ndarray         # int32
     mesh_surface: np.ndarray  # source surface id (in the layout mesh) per entry
+    ekind: np.ndarray = None  # (ne+ng,) uint8 element kinds (0 tri, 1 quad, 2 tet)
     inner: np.ndarray | None = None   # per color: surfaces before the ghost-touching ones
 
     @property
@@ -212,8 +259,9 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
     if (np.diff(colors) < 0).any():
         raise ValueError("surfaces must be grouped by color (apply a ReorderingPlan first)")
     X = unwrapped_element_coords(mesh, period)
-    detj, jinv = element_geometry(kind, X)
-    cen = X.mean(axis=1)
+    ekind = element_kinds(mesh)
+    detj, jinv = element_geometry(kind, X, ekind)
+    cen = element_centroids(mesh, X)
 
     ns = mesh.n_surfaces
     sid = np.arange(ns)
@@ -270,11 +318,13 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
         code_r = np.zeros(len(sid), dtype=np.int64)
         code_r[has_r] = _side_codes_tet(mesh.elem_verts, R[has_r], loc_r[has_r], sv[has_r])
     else:
-        code_l = _side_codes_2d(kind, mesh.elem_verts, L, loc_l, sv)
+        code_l = _side_codes_any(kind, ekind, mesh.elem_verts, L, loc_l, sv)
         code_r = np.zeros(len(sid), dtype=np.int64)
-        code_r[conf_r] = _side_codes_2d(kind, mesh.elem_verts, R[conf_r], loc_r[conf_r], sv[conf_r])
+        code_r[conf_r] = _side_codes_any(kind, ekind, mesh.elem_verts, R[conf_r], loc_r[conf_r],
+                                         sv[conf_r])
         if mortar_r.any():
-            code_r[mortar_r] = _side_codes_2d(kind, mesh.elem_verts, R[mortar_r], loc_r[mortar_r],
+            code_r[mortar_r] = _side_codes_any(kind, ekind, mesh.elem_verts, R[mortar_r],
+                                               loc_r[mortar_r],
                                               sv[mortar_r], mids=mid_of[sid[mortar_r]])
 
     # surface vertex coordinates as seen by the left element (unwrapped)
@@ -358,4 +408,4 @@ def build_surface_list(mesh: Mesh, colors: np.ndarray, n_colors: int,
         left=L.astype(np.int32), right=np.where(has_r, R, -1).astype(np.int32),
         code=code.astype(np.uint32), geom=np.ascontiguousarray(geom),
         jinv=np.ascontiguousarray(jinv), detj=detj, slot_ptr=ptr,
-        slots=slot.astype(np.int32), mesh_surface=sid, inner=inner)
+        slots=slot.astype(np.int32), mesh_surface=sid, inner=inner, ekind=ekind)

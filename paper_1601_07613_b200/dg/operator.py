@@ -30,10 +30,11 @@ from ..amr import RefinedMesh
 from ..coloring import SurfaceColoring, color
 from ..mesh import ElementKind, Mesh
 from ..reorder import ReorderingPlan, apply_plan, build_plan
-from .basis import DIM, REF_MEASURE, evaluate_basis, reference_tables, volume_rule
-from .layout import build_surface_list, mesh_kind, unwrapped_element_coords
+from .basis import DIM, HYBRID, REF_MEASURE, evaluate_basis, reference_tables, volume_rule
+from .layout import (build_surface_list, element_centroids, element_kinds, mesh_kind,
+                     unwrapped_element_coords)
 
-_KIND_CODE = {ElementKind.TRIANGLE: 0, ElementKind.QUAD: 1, ElementKind.TET: 2}
+_KIND_CODE = {ElementKind.TRIANGLE: 0, ElementKind.QUAD: 1, ElementKind.TET: 2, HYBRID: 3}
 _STRATEGY = {"colored": 0, "buffered": 1, "atomic": 2}
 # tets: sort colors >= 2 by side codes inside windows of 4096 surfaces (warps
 # read the same face-table rows; the element order survives at a coarse
@@ -100,7 +101,7 @@ def sfc_plan(mesh: Mesh, coloring: SurfaceColoring, period=None) -> ReorderingPl
         return full
     colors = np.asarray(coloring.colors)
     left, right = mesh.surf_elems[:, 0], mesh.surf_elems[:, 1]
-    cen = unwrapped_element_coords(mesh, period).mean(axis=1)
+    cen = element_centroids(mesh, unwrapped_element_coords(mesh, period))
     ones = np.flatnonzero(colors == 1)
     mid = cen[left[ones]].copy()
     inner = right[ones] >= 0
@@ -247,7 +248,8 @@ class DGOperator:
             slots=np.ascontiguousarray(sl.slots, dtype=np.int32),
             fphi=np.ascontiguousarray(t.face_phi), fw=np.ascontiguousarray(t.face_w),
             vphi=np.ascontiguousarray(t.vol_phi), vdphi=np.ascontiguousarray(t.vol_dphi),
-            vw=np.ascontiguousarray(t.vol_w))
+            vw=np.ascontiguousarray(t.vol_w),
+            ekind=np.ascontiguousarray(sl.ekind, dtype=np.uint8))
         d = _native.DGDesc()
         d.kind = _KIND_CODE[self.kind]
         d.physics = 0 if self.physics == "advection" else 1
@@ -266,6 +268,7 @@ class DGOperator:
         d.vol_phi, d.vol_dphi, d.vol_w = P(keep["vphi"]), P(keep["vdphi"]), P(keep["vw"])
         d.gamma = self.gamma
         d.state_f32 = 1 if self.state == "f32" else 0
+        d.elem_kind = P(keep["ekind"]) if self.kind is HYBRID else None
         for k in range(3):
             d.velocity[k] = self.velocity[k]
         ff = list(self.farfield) + [0.0] * (5 - len(self.farfield))
@@ -514,21 +517,33 @@ class DGOperator:
         return unwrapped_element_coords(self.mesh, self.period)
 
     def project(self, fn) -> np.ndarray:
-        """L2 projection of fn(x (n, dim)) -> (n, neq) (user order)."""
+        """L2 projection of fn(x (n, dim)) -> (n, neq) (user order).  Hybrid
+        meshes: each element on its own basis (triangles zero beyond their
+        N_p)."""
         X = self.element_coords()
-        pts, w = volume_rule(self.kind, self.degree + 1)
-        phi, _ = evaluate_basis(self.kind, self.degree, pts)
-        if self.kind is ElementKind.QUAD:
-            J = np.stack([X[:, 1] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)
+        out = np.zeros((self.mesh.n_elements, self.n_equations, self.n_basis))
+        if self.kind is HYBRID:
+            ek = element_kinds(self.mesh)
+            parts = [(ek == 0, ElementKind.TRIANGLE), (ek == 1, ElementKind.QUAD)]
         else:
-            J = np.stack([X[:, r + 1] - X[:, 0] for r in range(self.dim)], axis=2)
-        out = np.empty((self.mesh.n_elements, self.n_equations, self.n_basis))
-        chunk = 1 << 16
-        for a in range(0, self.mesh.n_elements, chunk):
-            b = min(a + chunk, self.mesh.n_elements)
-            x = X[a:b, 0][:, None, :] + np.einsum("erk,qk->eqr", J[a:b], pts)
-            vals = fn(x.reshape(-1, self.dim)).reshape(b - a, len(w), self.n_equations)
-            out[a:b] = np.einsum("q,qj,eqk->ekj", w, phi, vals)
+            parts = [(np.ones(self.mesh.n_elements, bool), self.kind)]
+        for sel, kind in parts:
+            idx = np.flatnonzero(sel)
+            if not len(idx):
+                continue
+            pts, w = volume_rule(kind, self.degree + 1)
+            phi, _ = evaluate_basis(kind, self.degree, pts)
+            Xk = X[idx]
+            if kind is ElementKind.QUAD:
+                J = np.stack([Xk[:, 1] - Xk[:, 0], Xk[:, 3] - Xk[:, 0]], axis=2)
+            else:
+                J = np.stack([Xk[:, r + 1] - Xk[:, 0] for r in range(self.dim)], axis=2)
+            chunk = 1 << 16
+            for a in range(0, len(idx), chunk):
+                b = min(a + chunk, len(idx))
+                x = Xk[a:b, 0][:, None, :] + np.einsum("erk,qk->eqr", J[a:b], pts)
+                vals = fn(x.reshape(-1, self.dim)).reshape(b - a, len(w), self.n_equations)
+                out[idx[a:b], :, :phi.shape[1]] = np.einsum("q,qj,eqk->ekj", w, phi, vals)
         return out
 
     def domain(self):
@@ -573,7 +588,12 @@ class DGOperator:
     def stable_dt(self, cfl: float = 0.1) -> float:
         """CFL-type step h / (max wave speed * (2p+1))."""
         detj = np.abs(self.surfaces.detj[: self.n_elements])
-        h = (detj / REF_MEASURE[self.kind]) ** (1.0 / self.dim)
+        if self.kind is HYBRID:
+            ref = np.where(self.surfaces.ekind[: self.n_elements] == 0,
+                           REF_MEASURE[ElementKind.TRIANGLE], REF_MEASURE[ElementKind.QUAD])
+        else:
+            ref = REF_MEASURE[self.kind]
+        h = (detj / ref) ** (1.0 / self.dim)
         ff = np.asarray(self.farfield)
         if self.physics == "advection":
             speed = np.linalg.norm(self.velocity[: self.dim]) + 1e-30
@@ -603,4 +623,5 @@ class DGOperator:
                     gamma=self.gamma, velocity=self.velocity, farfield=self.farfield,
                     vertices=m.vertices, elem_verts=m.elem_verts, surf_verts=m.surf_verts,
                     surf_elems=surf_elems, colors=np.asarray(self.coloring.colors),
-                    n_colors=int(self.coloring.n_colors), active=active, period=self.period)
+                    n_colors=int(self.coloring.n_colors), active=active, period=self.period,
+                    elem_kind=np.asarray(m.elem_kind) if self.kind is HYBRID else None)

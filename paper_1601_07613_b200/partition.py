@@ -31,8 +31,8 @@ from .mesh import Mesh
 
 def slab_owner(mesh: Mesh, world: int, axis: int | None = None, period=None) -> np.ndarray:
     """Rank of every element: equal-count slabs of centroid coordinate."""
-    from .dg.layout import unwrapped_element_coords
-    cen = unwrapped_element_coords(mesh, period).mean(axis=1)
+    from .dg.layout import element_centroids, unwrapped_element_coords
+    cen = element_centroids(mesh, unwrapped_element_coords(mesh, period))
     if axis is None:
         axis = 0 if mesh.dim == 3 else 1
     order = np.argsort(cen[:, axis], kind="stable")

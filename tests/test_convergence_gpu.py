@@ -50,6 +50,35 @@ def wave_error(gen, n, p, physics):
     return float(np.sqrt((detj[:, None] * err ** 2).sum()))
 
 
+def gen_hybrid_periodic(n):
+    """Periodic conforming triangle + quad mix (cells with even i+j split
+    into two triangles, the others quads; conftest.hybrid_patch layout)."""
+    from paper_1601_07613_b200.generators import _cell_corners, _lattice
+    from paper_1601_07613_b200.mesh import MAX_ELEM_VERTS
+    coords, table = _lattice(n, n, True, True)
+    i, j, a, b, c, d = _cell_corners(table, n, n)
+    rows, kinds = [], []
+    for k in range(len(a)):
+        if (i[k] + j[k]) % 2 == 0:
+            rows += [(a[k], b[k], c[k], -1), (a[k], c[k], d[k], -1)]
+            kinds += [0, 0]
+        else:
+            rows.append((a[k], b[k], c[k], d[k]))
+            kinds.append(1)
+    ev = np.asarray(rows, dtype=np.int64).reshape(-1, MAX_ELEM_VERTS)
+    return P.assemble(coords, np.asarray(kinds, np.int8), ev)
+
+
+@pytest.mark.parametrize("gen,physics,p", [
+    (gen_hybrid_periodic, "advection", 2),
+    (gen_hybrid_periodic, "euler", 2),
+    (gen_hybrid_periodic, "euler", 3),
+], ids=["hybrid-adv-p2", "hybrid-euler-p2", "hybrid-euler-p3"])
+def test_hybrid_convergence_rate(cuda, gen, physics, p):
+    """Triangle + quad meshes converge at the design order too."""
+    test_convergence_rate(cuda, gen, physics, p)
+
+
 @pytest.mark.parametrize("gen,physics,p", [
     (lambda n: P.gen_tri_rect(n, n, (True, True)), "advection", 1),
     (lambda n: P.gen_tri_rect(n, n, (True, True)), "advection", 2),

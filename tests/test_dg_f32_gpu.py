@@ -17,6 +17,8 @@ TOL32 = 1e-5
 CASES = [
     ("tri-p2", lambda: P.shuffle_elements(P.gen_tri_rect(16, 13), 0), 2, 0),
     ("quad-p3", lambda: P.gen_quad_rect(12, 10), 3, 1),
+    # two lanes per side with an odd basis size: lane runs only 8-byte aligned
+    ("quad-p2", lambda: P.shuffle_elements(P.gen_quad_rect(11, 9), 1), 2, 1),
     ("tet-p2", lambda: P.gen_tet_prism(5, 4, 4), 2, 1),
     ("tet-p1", lambda: P.shuffle_elements(P.gen_tet_prism(4, 4, 3), 2), 1, 0),
 ]

@@ -104,3 +104,46 @@ def test_quadrature_exactness(kind, p):
         else:
             exact = np.prod([factorial(k) for k in e]) / factorial(sum(e) + dim)
         assert abs(num - exact) < 1e-14, (e, num, exact)
+
+
+# ---------------------------------------------------- hybrid (tri + quad)
+def hybrid_problem(mesh, col, p, phys, kinds=None):
+    ek = np.asarray(mesh.elem_kind if kinds is None else kinds)
+    return D.Problem("hybrid", p, phys, mesh.vertices, mesh.elem_verts, mesh.surf_verts,
+                     mesh.surf_elems, col.colors, col.n_colors, np.ones(mesh.n_surfaces, bool),
+                     elem_kind=ek)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_hybrid_free_stream_preservation(p):
+    from conftest import hybrid_patch
+    mesh = hybrid_patch(5, 4)
+    col, _ = P.color(mesh)
+    U0 = (1.0, 0.3, -0.2, 2.5)
+    pr = hybrid_problem(mesh, col, p, D.Physics("euler", 2, farfield=U0))
+    U = D.project(pr, lambda x: np.tile(U0, (len(x), 1)))
+    tri = np.asarray(mesh.elem_kind) == 0
+    assert np.abs(U[tri][:, :, (p + 1) * (p + 2) // 2:]).max() == 0.0
+    assert np.abs(D.rhs(pr, U)).max() < 1e-12
+
+
+@pytest.mark.parametrize("kind,p", [("tri", 2), ("quad", 2), ("tri", 3)])
+def test_hybrid_layout_of_a_single_kind_mesh_matches_that_kind(kind, p):
+    """A pure mesh described as "hybrid" (every element of one kind, the
+    coefficients quad-sized) gives the single-kind operator's residual."""
+    mesh = P.gen_tri_rect(5, 4) if kind == "tri" else P.gen_quad_rect(4, 3)
+    col, _ = P.color(mesh)
+    ph = D.Physics("euler", 2, farfield=(1.0, 0.3, 0.1, 2.5))
+    single = problem(mesh, col, kind, p, ph)
+    hyb = hybrid_problem(mesh, col, p, ph)
+    rng = np.random.default_rng(1)
+    nb = D.Basis(kind, p).scale.size
+    U = rng.normal(size=(mesh.n_elements, 4, nb)) * 0.05
+    U[:, 0, 0] += 1.5
+    U[:, 3, 0] += 4.0
+    Uh = np.zeros((mesh.n_elements, 4, (p + 1) ** 2))
+    Uh[:, :, :nb] = U
+    want = D.rhs(single, U)
+    got = D.rhs(hyb, Uh)
+    assert np.abs(got[:, :, nb:]).max(initial=0.0) == 0.0
+    assert np.abs(got[:, :, :nb] - want).max() < 1e-13 * np.abs(want).max()

@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     lib = _native.lib()
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.mc_abi_version() == 1010
+    assert lib.mc_abi_version() == 1011
     assert lib.mc_device_count() >= 0
 
 
