@@ -368,6 +368,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--layouts", action="store_true",
                     help="time the paper's Table 7 layouts on c2 instead")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "push"],
+                    help="N>1 ghost exchange: NCCL send/recv of kernel-packed rows (default) "
+                         "or the peer push fused into the last-touch kernel (symmetric memory)")
     ap.add_argument("--state", default="f64", choices=["f64", "f32"],
                     help="element-block storage (f32: half the bytes, fp64 arithmetic, the north "
                          "star's 1e-5 tolerance; not the headline)")
@@ -409,11 +412,19 @@ def main():
     if world > 1:                      # one global time step; also initialises NCCL P2P
         dt = reduce_scalar(dt, dist.ReduceOp.MIN)
         dist.barrier()
-    U = op.to_device(U_host)
+    push = world > 1 and args.exchange == "push"
+    if push:   # exchange fused into the last-touch kernel over NVLink peer memory
+        from paper_1601_07613_b200.partition import setup_symmetric_push
+        U, push_fill, push_barrier = setup_symmetric_push(op)
+        U[: op.n_elements] = op.to_device(U_host)[: op.n_elements]
+        push_fill()
+    else:
+        U = op.to_device(U_host)
     work = op.work_device()
     U0, R = work[0], work[1]
     stream = torch.cuda.current_stream()
     nc = op.n_colors
+    stage_no = [0]
 
     def mark(events, mode, a, c):
         if events is not None:
@@ -427,6 +438,11 @@ def main():
                 for c in range(1, nc + 1):
                     mark(events, mode, a, c)
                     op.color_pass_device(c, U, U0, R, mode, a, b, dt, stream)
+                continue
+            if push:   # ghosts pushed by the peers' last touches; one barrier per stage
+                op.stage_push(U, U0, R, mode, a, b, dt, stage_no[0], push_barrier, stream,
+                              marker=lambda c, m=mode, aa=a: mark(events, m, aa, c))
+                stage_no[0] += 1
                 continue
             # ghost exchange overlapped with the ghost-free part of color 1;
             # the send rows were packed by the previous stage's last touches
@@ -511,7 +527,11 @@ def main():
         for _ in range(args.e2e_steps):
             dev_user.copy_(pinned, non_blocking=True)
             op.user_to_device(dev_user, U)
-            op.ssprk3_distributed(U, work, dt, 1)
+            if push:
+                push_fill(stage_no[0] % 2)
+                stage_no[0] = op.ssprk3_push(U, work, dt, 1, push_barrier, stage0=stage_no[0])
+            else:
+                op.ssprk3_distributed(U, work, dt, 1)
             op.device_to_user(U, dev_user)
             pinned.copy_(dev_user, non_blocking=True)
             torch.cuda.synchronize()
@@ -554,8 +574,11 @@ def main():
                          f"{op.n_local * op.stride * (4 if args.state == 'f32' else 8) / 1e9:.2f}"
                          " GB x 3 arrays, no flush needed)",
                    "parallelism": "single-GPU" if world == 1 else
-                   f"domain decomposition x{world} (slabs, {backend.upper()} ghost exchange per "
-                   f"stage{'' if backend == 'nccl' else ', host-staged: functional run only'})",
+                   (f"domain decomposition x{world} (slabs, ghost blocks pushed into the peers' "
+                    "double-buffered ghost rows by the last-touch kernel over NVLink symmetric "
+                    "memory, one device barrier per stage)" if push else
+                    f"domain decomposition x{world} (slabs, {backend.upper()} ghost exchange per "
+                    f"stage{'' if backend == 'nccl' else ', host-staged: functional run only'})"),
                    "setup_s": round(t_setup, 2)},
         "dof_updates_per_s": dof_rate,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -249,6 +249,22 @@ int mc_dg_color_range_pass(mc_dg* dg, int color, int64_t begin, int64_t end,
  * NULL turns it off. */
 int mc_dg_set_send_rows(mc_dg* dg, const int32_t* slot_host, double* send_buf_dev,
                         int64_t n_slots);
+/* Peer-push ghost exchange (partitioned runs on one NVLink/NVSwitch node):
+ * dst[ptr[e] .. ptr[e+1]) are byte addresses, valid in this process (peer
+ * memory mapped by the caller, e.g. symmetric memory), of the rows that
+ * owned element e's block must land in on the peers; every last-touch pass
+ * of an RK stage stores e's updated block there (+ the push parity's row
+ * shift) as it writes U — the exchange is fused into the kernel, no send
+ * buffer, no copy engine.  ptr = NULL turns it off.  Register kernels only. */
+int mc_dg_set_push_rows(mc_dg* dg, const int64_t* ptr_host, const uint64_t* dst_host,
+                        int64_t nnz);
+/* Double-buffered ghost rows for the peer push: ghost g (id ne + g in the
+ * surface list) lives at rows ne + 2g (parity 0) and ne + 2g + 1 (parity 1)
+ * of U; launches read read_parity (-1: the plain layout, ghost g at row
+ * ne + g) and push into the peers' push_parity rows.  A stage reads the
+ * parity its peers pushed in the previous stage and pushes the other one,
+ * so a peer still reading this stage's ghosts is never overwritten. */
+int mc_dg_set_ghost_parity(mc_dg* dg, int read_parity, int push_parity);
 /* n_steps SSP-RK3 steps; work_dev = 2 blocks arrays (U0, R scratch). */
 int mc_dg_ssprk3(mc_dg* dg, double* U_dev, double* work_dev, double dt,
                  int n_steps, void* stream);

@@ -104,6 +104,8 @@ _SIGS = {
     "mc_dg_ssprk3_host": (C.c_int, [_P, _P, C.c_double, C.c_int]),
     "mc_dg_set_grid_cap": (C.c_int, [_P, C.c_int]),
     "mc_dg_set_send_rows": (C.c_int, [_P, _P, _P, _I64]),
+    "mc_dg_set_push_rows": (C.c_int, [_P, _P, _P, _I64]),
+    "mc_dg_set_ghost_parity": (C.c_int, [_P, C.c_int, C.c_int]),
     "mc_dg_set_user_rows": (C.c_int, [_P, _P, _I64]),
     "mc_dg_user_to_internal": (C.c_int, [_P, _P, _P, _P]),
     "mc_dg_internal_to_user": (C.c_int, [_P, _P, _P, _P]),

@@ -48,6 +48,8 @@ struct mc_dg {
   double* d_user = nullptr;        // user-layout staging (n_user_rows x W)
   double* d_user_R = nullptr;      // user-layout residual staging
   int32_t* d_send_slot = nullptr;  // per owned element: ghost send-buffer slot or -1
+  int64_t* d_push_ptr = nullptr;   // peer push: CSR of destinations per owned element
+  unsigned long long* d_push_dst = nullptr;
 };
 
 namespace {
@@ -334,6 +336,7 @@ MC_API int mc_dg_create(const mc_dg_desc* d, mc_dg** out) {
   v.geom = h->d_geom;
   v.jinv = h->d_jinv;
   v.ekind = h->d_ekind;
+  v.ghost_par = -1;
   v.tables = h->d_tables;
   v.slot_ptr = h->d_slot_ptr;
   v.slots = h->d_slots;
@@ -365,6 +368,8 @@ MC_API int mc_dg_destroy(mc_dg* h) {
   cudaFree(h->d_user);
   cudaFree(h->d_user_R);
   cudaFree(h->d_send_slot);
+  cudaFree(h->d_push_ptr);
+  cudaFree(h->d_push_dst);
   if (h->step_exec) cudaGraphExecDestroy(h->step_exec);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -558,6 +563,44 @@ MC_API int mc_dg_set_send_rows(mc_dg* h, const int32_t* slot, double* send_buf_d
   DG_TRY(upload(&h->d_send_slot, slot, h->ne));
   h->view.send_slot = h->d_send_slot;
   h->view.send_buf = send_buf_dev;
+  return MC_OK;
+}
+
+MC_API int mc_dg_set_push_rows(mc_dg* h, const int64_t* ptr, const uint64_t* dst, int64_t nnz) {
+  if (!h) return mc_fail(MC_EINVAL, "null argument");
+  cudaFree(h->d_push_ptr);
+  cudaFree(h->d_push_dst);
+  h->d_push_ptr = nullptr;
+  h->d_push_dst = nullptr;
+  h->view.push_ptr = nullptr;
+  h->view.push_dst = nullptr;
+  if (h->step_exec) {
+    cudaGraphExecDestroy(h->step_exec);
+    h->step_exec = nullptr;
+  }
+  if (!ptr) return MC_OK;
+  if (!h->ops->tpe) return mc_fail(MC_EUNSUPPORTED, "peer push needs the register kernels");
+  if (ptr[0] != 0 || ptr[h->ne] != nnz || nnz < 0)
+    return mc_fail(MC_EINVAL, "push CSR does not cover the destinations");
+  for (int64_t e = 0; e < h->ne; ++e)
+    if (ptr[e + 1] < ptr[e]) return mc_fail(MC_EINVAL, "push CSR must be non-decreasing");
+  const uint64_t align = h->f32 ? 16 : 32;
+  for (int64_t k = 0; k < nnz; ++k)
+    if (!dst[k] || dst[k] % align)
+      return mc_fail(MC_EINVAL, "push destination " + std::to_string(k) + " is null or misaligned");
+  DG_TRY(upload(&h->d_push_ptr, ptr, h->ne + 1));
+  DG_TRY(upload(&h->d_push_dst, reinterpret_cast<const unsigned long long*>(dst), nnz));
+  h->view.push_ptr = h->d_push_ptr;
+  h->view.push_dst = h->d_push_dst;
+  return MC_OK;
+}
+
+MC_API int mc_dg_set_ghost_parity(mc_dg* h, int read_parity, int push_parity) {
+  if (!h) return mc_fail(MC_EINVAL, "null argument");
+  if (read_parity < -1 || read_parity > 1 || push_parity < 0 || push_parity > 1)
+    return mc_fail(MC_EINVAL, "parities must be -1/0/1 (read) and 0/1 (push)");
+  h->view.ghost_par = read_parity;
+  h->view.push_shift = int64_t(push_parity) * h->stride;
   return MC_OK;
 }
 

@@ -226,6 +226,17 @@ struct View {
   // buffer (send_slot[e] >= 0), so the next stage posts it without a pack
   const int32_t* send_slot;
   void* send_buf;          // element blocks of the state type (double / float)
+  // peer-push exchange (mc_dg_set_push_rows): the last-touch pass also
+  // stores every interface element's new block straight into its rows in
+  // the peers' state arrays (NVLink P2P stores through mapped peer memory),
+  // push_dst[push_ptr[e] .. push_ptr[e+1]) byte addresses, + push_shift
+  // state values (the ghost copy the peers read next stage).  ghost_par
+  // >= 0: ghost rows are double-buffered (ghost g at rows ne + 2g + parity)
+  // and this launch reads parity ghost_par
+  const int64_t* push_ptr;
+  const unsigned long long* push_dst;
+  int64_t push_shift;
+  int ghost_par;
 };
 
 struct RK {

@@ -524,6 +524,7 @@ __device__ __forceinline__ TpeSide tpe_side(const View& v, int64_t s, int64_t en
     t.scale = __ldg(gm + C::DIM + side);
   }
   t.boundary = R < 0;
+  if (v.ghost_par >= 0 && R >= v.n_elements) R = int(v.n_elements + 2 * (R - v.n_elements) + v.ghost_par);
   t.e = side ? R : L;
   t.has = t.valid && t.e >= 0;
   t.owner = t.has && !(side && (t.code & MC_FLAG_R_GHOST));
@@ -551,6 +552,8 @@ __device__ __forceinline__ TpeSide tpe_side_pre(const View& v, int64_t s, int64_
     for (int d = 0; d < C::DIM; ++d) t.n[d] = __ldg(gm + d);
     t.scale = __ldg(gm + C::DIM + side);
   }
+  if (v.ghost_par >= 0 && e_pre >= v.n_elements)   // double-buffered ghost rows
+    e_pre = int(v.n_elements + 2 * (e_pre - v.n_elements) + v.ghost_par);
   t.e = t.valid ? e_pre : -1;
   t.boundary = side && t.e < 0;
   t.has = t.valid && t.e >= 0;
@@ -1275,6 +1278,13 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
           const int sl = __ldg(v.send_slot + t.e);
           if (sl >= 0)
             sstore<WH, kWhole, T::V4>(static_cast<S*>(v.send_buf) + int64_t(sl) * v.stride + ln.eq0 * C::NP, n, acc);
+        }
+        if (v.push_ptr) {   // peer push: the new block into the peers' ghost rows
+          const int64_t k1 = __ldg(v.push_ptr + t.e + 1);
+          for (int64_t k = __ldg(v.push_ptr + t.e); k < k1; ++k) {
+            S* d = reinterpret_cast<S*>(__ldg(v.push_dst + k)) + v.push_shift + ln.eq0 * C::NP;
+            sstore<WH, kWhole, T::V4>(d, n, acc);
+          }
         }
       } else {
         sstore<WH, kWhole, T::V4>(R + off, n, acc);

@@ -443,6 +443,66 @@ class DGOperator:
         if self.halo is not None:
             self.halo.stage_done(rk=mode != 0)
 
+    # ------------------------------------------------ peer-push exchange
+    def enable_push(self, layout: dict, bases: dict) -> None:
+        """Fuse the ghost exchange into the last-touch kernel
+        (``partition.HaloPush``): ``layout[q] = (n_owned_q, recv_q)`` for the
+        peers, ``bases[q]`` the mapped address of peer q's state array
+        (``HaloPush.state_rows`` rows)."""
+        from ..partition import HaloPush
+        if self.part is None:
+            raise ValueError("peer push needs a partitioned operator")
+        sl = self.surfaces
+        last1 = sl.code[sl.bounds[0]:sl.bounds[1]] & ((1 << 13) | (1 << 15))
+        if last1.any():
+            raise NotImplementedError("an element's last touch in color 1 (its inner part "
+                                      "runs before the stage barrier)")
+        self.push = HaloPush(self.part, layout)
+        esize = 4 if self.state == "f32" else 8
+        ptr, dst = self.push.destinations(bases, self.stride, esize)
+        _native.check(self._lib.mc_dg_set_push_rows(self._h, _native.ptr(ptr), _native.ptr(dst),
+                                                    int(len(dst))))
+
+    def push_state_device(self):
+        """A zeroed state array with double-buffered ghost rows."""
+        import torch
+        from ..partition import HaloPush
+        return torch.zeros((HaloPush.state_rows(self.part), self.stride), dtype=self.torch_dtype,
+                           device="cuda")
+
+    def stage_push(self, U_dev, U0_dev, R_dev, mode: int, a: float, b: float, dt: float,
+                   stage: int, barrier=None, stream=None, marker=None) -> None:
+        """One SSP-RK stage with the peer-push exchange: the part of color 1
+        that touches no ghost, the stage barrier (every rank finished stage
+        ``stage - 1``, so the ghost copy of parity ``stage % 2`` is complete
+        and no peer still reads the other copy), then the rest; last-touch
+        passes push parity ``(stage + 1) % 2``."""
+        import torch
+        cs = stream if stream is not None else torch.cuda.current_stream()
+        _native.check(self._lib.mc_dg_set_ghost_parity(self._h, stage % 2, (stage + 1) % 2))
+        if marker:
+            marker(1)
+        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, cs, part="inner")
+        if barrier is not None:
+            with torch.cuda.stream(cs):
+                barrier()
+        self.color_pass_device(1, U_dev, U0_dev, R_dev, mode, a, b, dt, cs, part="interface")
+        for c in range(2, self.n_colors + 1):
+            if marker:
+                marker(c)
+            self.color_pass_device(c, U_dev, U0_dev, R_dev, mode, a, b, dt, cs)
+
+    def ssprk3_push(self, U_dev, work_dev, dt: float, steps: int = 1, barrier=None,
+                    stream=None, stage0: int = 0) -> int:
+        """SSP-RK3 with the peer push; returns the next stage index."""
+        U0, R = work_dev[0], work_dev[1]
+        s = stage0
+        for _ in range(steps):
+            for mode, a, b in self.STAGES:
+                self.stage_push(U_dev, U0, R, mode, a, b, dt, s, barrier, stream)
+                s += 1
+        return s
+
     def work_device(self):
         import torch
         return torch.zeros((2, self.n_local, self.stride), dtype=self.torch_dtype, device="cuda")

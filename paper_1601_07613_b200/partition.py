@@ -267,3 +267,108 @@ class HaloExchange:
 
     def exchange(self, U) -> None:
         self.finish(U, self.start(U))
+
+
+class HaloPush:
+    """Peer-push ghost exchange fused into the last-touch kernel (one node,
+    NVLink / NVSwitch peer memory): instead of packing a send buffer and
+    posting NCCL transfers, every rank's last-touch pass of an RK stage
+    stores each interface element's updated block straight into the peers'
+    ghost rows (``mc_dg_set_push_rows``).  Ghost rows are double-buffered
+    (ghost g at rows n_owned + 2g + parity, ``mc_dg_set_ghost_parity``):
+    stage s reads parity s % 2 and pushes parity (s + 1) % 2, so with one
+    barrier per stage (all ranks finished stage s - 1) no rank can
+    overwrite ghosts a peer is still reading.  The state array therefore
+    has ``n_owned + 2 * n_ghosts`` rows.
+
+    ``layout[q] = (n_owned_q, recv_q)`` describes every peer q (its owned
+    count and its ``Partition.recv``), which each rank learns with one
+    ``all_gather_object`` (or, emulated, from the other ranks' partitions)."""
+
+    def __init__(self, part: Partition, layout: dict):
+        self.part = part
+        self.layout = layout
+        self.peers = sorted(part.send)
+        for q in self.peers:
+            if part.rank not in layout[q][1]:
+                raise ValueError(f"peer {q} receives nothing from rank {part.rank}")
+
+    @staticmethod
+    def state_rows(part: Partition) -> int:
+        return part.n_owned + 2 * len(part.ghosts)
+
+    def ghost_row(self, q: int, k: int, parity: int = 0) -> int:
+        """Row of peer q's state array holding the k-th block this rank
+        sends q (q's ghost order), in the given parity copy."""
+        ne_q, recv_q = self.layout[q]
+        a_q, _ = recv_q[self.part.rank]
+        return ne_q + 2 * (a_q - ne_q + k) + parity
+
+    def destinations(self, bases: dict, stride: int, esize: int):
+        """CSR (ptr (n_owned+1,), dst (nnz,) uint64 byte addresses of the
+        parity-0 rows) for ``mc_dg_set_push_rows``; ``bases[q]`` = the
+        address of peer q's state array as mapped in this process."""
+        per = [[] for _ in range(self.part.n_owned)]
+        for q in self.peers:
+            for k, e in enumerate(self.part.send[q]):
+                per[int(e)].append(int(bases[q]) + self.ghost_row(q, k) * stride * esize)
+        ptr = np.zeros(self.part.n_owned + 1, dtype=np.int64)
+        ptr[1:] = np.cumsum([len(x) for x in per])
+        dst = np.asarray([a for x in per for a in x], dtype=np.uint64)
+        return ptr, dst
+
+    def fill(self, U, peers: dict, parity: int = 0) -> None:
+        """Write this rank's current interface blocks into the peers' ghost
+        rows of the given parity (``peers[q]``: a tensor view of peer q's
+        state array, mapped peer memory); the run's first stage needs it."""
+        import torch
+        for q in self.peers:
+            rows = torch.as_tensor([self.ghost_row(q, k, parity)
+                                    for k in range(len(self.part.send[q]))],
+                                   dtype=torch.int64, device=U.device)
+            src = torch.as_tensor(self.part.send[q], dtype=torch.int64, device=U.device)
+            peers[q].index_copy_(0, rows, U.index_select(0, src))
+
+
+def setup_symmetric_push(op, group=None):
+    """Multi-GPU wiring of ``HaloPush`` on one node: the state array is
+    allocated in torch symmetric memory (every rank maps every peer's copy
+    over NVLink / NVSwitch), peer layouts are exchanged once, the
+    operator's last-touch kernel gets the peers' ghost-row addresses, and
+    the stage barrier is symmetric memory's device-side barrier (signal
+    pads, no host round trip).  Returns ``(U, fill, barrier)``:
+    ``fill(parity)`` writes this rank's current interface blocks into the
+    peers' ghost rows of that parity and waits for every rank (call it
+    after loading a state, with the parity ``stage % 2`` of the next
+    ``stage_push``); ``barrier()`` is the
+    per-stage barrier for ``stage_push``.  Single node only; written for an
+    8-GPU NVSwitch box, exercised here only through the single-process
+    emulation (tests/test_partition_gpu.py)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    group = group or dist.group.WORLD
+    rows = torch.tensor([HaloPush.state_rows(op.part)], device="cuda")
+    dist.all_reduce(rows, op=dist.ReduceOp.MAX, group=group)
+    if hasattr(symm_mem, "enable_symm_mem_for_group"):
+        try:
+            symm_mem.enable_symm_mem_for_group(group.group_name)
+        except Exception:
+            pass
+    U = symm_mem.empty(int(rows.item()), op.stride, dtype=op.torch_dtype, device="cuda")
+    U.zero_()
+    hdl = symm_mem.rendezvous(U, group)
+    infos = [None] * dist.get_world_size(group)
+    dist.all_gather_object(infos, (op.part.n_owned, op.part.recv), group=group)
+    peers = sorted(op.part.send)
+    op.enable_push({q: infos[q] for q in peers}, {q: int(hdl.buffer_ptrs[q]) for q in peers})
+    views = {q: hdl.get_buffer(q, tuple(U.shape), U.dtype) for q in peers}
+
+    def barrier():
+        hdl.barrier(channel=0)
+
+    def fill(parity: int = 0):
+        op.push.fill(U, views, parity)
+        barrier()
+
+    return U, fill, barrier

@@ -232,3 +232,30 @@ def test_three_rank_exchange_with_kernel_packed_send_rows(tmp_path):
     mp.spawn(_worker_packed, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     for r in range(world):
         assert np.load(tmp_path / f"ok{r}.npy").all()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_peer_push_destinations(world):
+    """HaloPush (exchange fused into the last-touch kernel): every pushed
+    block lands in the peer's ghost row of the same global element, in the
+    double-buffered layout (ghost g at n_owned + 2g + parity)."""
+    from paper_1601_07613_b200.partition import HaloPush
+    lm, lc = layout_case()
+    owner = slab_owner(lm, world)
+    parts = [build_partition(lm, lc.colors, lc.n_colors, owner, r) for r in range(world)]
+    layout = {r: (p.n_owned, p.recv) for r, p in enumerate(parts)}
+    stride, esize = 24, 8
+    bases = {q: (q + 1) << 32 for q in range(world)}
+    for p in parts:
+        hp = HaloPush(p, {q: layout[q] for q in p.send})
+        ptr, dst = hp.destinations({q: bases[q] for q in p.send}, stride, esize)
+        assert ptr[-1] == len(dst) == sum(len(v) for v in p.send.values())
+        for e in range(p.n_owned):
+            for addr in dst[ptr[e]:ptr[e + 1]]:
+                q = (int(addr) >> 32) - 1
+                row = (int(addr) - bases[q]) // (stride * esize)
+                ne_q = parts[q].n_owned
+                assert row >= ne_q and (row - ne_q) % 2 == 0
+                g = (row - ne_q) // 2
+                assert parts[q].ghosts[g] == p.owned[e]
+        assert HaloPush.state_rows(p) == p.n_owned + 2 * len(p.ghosts)

@@ -181,3 +181,47 @@ def test_partitioned_amr_matches_single_domain(cuda, world, levels):
         rows = Ud[: op.n_elements, : op.block_width()].cpu().numpy()
         got[op.owned_user_ids()] = rows.reshape(op.n_elements, op.n_equations, op.n_basis)
     assert np.array_equal(got, want), np.abs(got - want).max()
+
+
+@pytest.mark.parametrize("world,kind", [(2, "tet"), (3, "tri"), (4, "tet")])
+def test_peer_push_exchange_matches_single_domain(cuda, world, kind):
+    """The exchange fused into the last-touch kernel (``HaloPush``): every
+    rank's last-touch passes store interface blocks straight into the
+    peers' double-buffered ghost rows (same-device buffers stand in for
+    mapped peer memory).  Ranks run each stage one after another (the
+    sequential order is the stage barrier); a rank running stage s after
+    its peers already pushed stage s + 1 ghosts must still read stage s's
+    copy, so a wrong parity would change the result.  Owned results equal
+    the single domain bit for bit."""
+    import torch
+    mesh = {"tri": lambda: P.shuffle_elements(P.gen_tri_rect(14, 11), 3),
+            "tet": lambda: P.gen_tet_prism(8, 3, 3)}[kind]()
+    col, _ = P.color(mesh)
+    single = DGOperator(mesh, col, degree=2, physics="euler")
+    U = single.initial_state("wave")
+    dt = single.stable_dt(0.2)
+    want = single.ssprk3(U, dt, 2)
+    ops = [DGOperator(mesh, col, degree=2, physics="euler", world=world, rank=r)
+           for r in range(world)]
+    layout = {r: (op.n_elements, op.part.recv) for r, op in enumerate(ops)}
+    Us = [op.push_state_device() for op in ops]
+    for op, Ud in zip(ops, Us):
+        Ud[: op.n_elements] = torch.from_numpy(op.to_internal(U)[: op.n_elements]).cuda()
+    for r, op in enumerate(ops):
+        op.enable_push({q: layout[q] for q in op.part.send},
+                       {q: Us[q].data_ptr() for q in op.part.send})
+    for r, op in enumerate(ops):                 # the run's first ghost copy (parity 0)
+        op.push.fill(Us[r], {q: Us[q] for q in op.part.send})
+    works = [op.work_device() for op in ops]
+    stage = 0
+    for _ in range(2):
+        for mode, a, b in DGOperator.STAGES:
+            for op, Ud, w in zip(ops, Us, works):
+                op.stage_push(Ud, w[0], w[1], mode, a, b, dt, stage)
+            stage += 1
+    torch.cuda.synchronize()
+    got = np.empty_like(want)
+    for op, Ud in zip(ops, Us):
+        rows = Ud[: op.n_elements, : op.block_width()].cpu().numpy()
+        got[op.owned_user_ids()] = rows.reshape(op.n_elements, op.n_equations, op.n_basis)
+    assert np.array_equal(got, want), np.abs(got - want).max()
