@@ -69,6 +69,9 @@ CONFIGS = {
            ("tet", (28, 28, 28), None)),
     "c5": ("2D Euler DG p=2, 1:4 refined disc r=177 in gen_tri_rect(708,708), 6 colors, "
            "mortars", "euler", 2, ("tri", (177, 177), None)),
+    # not a BASELINE config: the hybrid (triangle + quad) layout at c2's scale
+    "h1": ("2D Euler DG p=2, gen_hybrid_rect(708,708) (triangles + quads, conftest."
+           "hybrid_patch layout), LF, 4 colors", "euler", 2, ("hybrid", (177, 177), None)),
 }
 
 
@@ -111,6 +114,7 @@ def config_spec(name: str, device: str | None = "cuda"):
         "c2": lambda: P.shuffle_elements(P.gen_tri_rect(708, 708, device=dv), 0, device=dv),
         "c3": lambda: P.gen_quad_rect(2000, 2000, device=dv),
         "c4": lambda: P.gen_tet_prism(110, 110, 110, device=dv),
+        "h1": lambda: P.gen_hybrid_rect(708, 708, device=dv),
     }
 
     def c5():
@@ -249,11 +253,12 @@ def oracle_sample(config: str):
     from oracle import dg_oracle as D
     from oracle import mesh_oracle as MO
     desc, physics, p, (kind, dims, shuffle) = CONFIGS[config]
-    gen = {"tri": MO.gen_tri_rect, "quad": MO.gen_quad_rect, "tet": MO.gen_tet_prism}[kind]
+    gen = {"tri": MO.gen_tri_rect, "quad": MO.gen_quad_rect, "tet": MO.gen_tet_prism,
+           "hybrid": MO.gen_hybrid_rect}[kind]
     m = gen(*dims)
     if shuffle is not None:
         m = MO.shuffle_elements(m, shuffle)
-    nc = 4 if kind in ("quad", "tet") else 3
+    nc = 4 if kind in ("quad", "tet", "hybrid") else 3
     cols, _ = CO.color(m["surf_elems"], m["elem_surfs"], nc, seed=0)
     dim = 3 if kind == "tet" else 2
     gamma = 1.4
@@ -266,7 +271,8 @@ def oracle_sample(config: str):
     phys = D.Physics(physics, dim, gamma=gamma, farfield=ff)
     ns = len(cols)
     prob = D.Problem(kind, p, phys, m["vertices"], m["elem_verts"], m["surf_verts"],
-                     m["surf_elems"], np.asarray(cols, dtype=np.int32), nc, np.ones(ns, bool))
+                     m["surf_elems"], np.asarray(cols, dtype=np.int32), nc, np.ones(ns, bool),
+                     elem_kind=np.asarray(m["elem_kind"]) if kind == "hybrid" else None)
     D.setup(prob)
     lo, hi = m["vertices"].min(axis=0), m["vertices"].max(axis=0)
 

@@ -117,6 +117,24 @@ def gen_quad_rect(nx, ny, periodic=False) -> dict:
     return assemble(verts, np.full(len(ev), QUAD, np.int8), ev)
 
 
+def gen_hybrid_rect(nx, ny, periodic=False) -> dict:
+    """Triangle + quad mix: the reference tests' ``conftest.hybrid_patch``
+    layout (cells with i+j even -> triangles (a,b,c), (a,c,d); others quads)."""
+    px, py = _pair(periodic)
+    verts, vid = _grid(nx, ny, px, py)
+    rows, kinds = [], []
+    for c in range(nx * ny):
+        j, i = divmod(c, nx)
+        a, b, cc, d = vid[j, i], vid[j, i + 1], vid[j + 1, i + 1], vid[j + 1, i]
+        if (i + j) % 2 == 0:
+            rows += [(a, b, cc, -1), (a, cc, d, -1)]
+            kinds += [TRI, TRI]
+        else:
+            rows.append((a, b, cc, d))
+            kinds.append(QUAD)
+    return assemble(verts, np.asarray(kinds, np.int8), np.asarray(rows, np.int64))
+
+
 # six tets per hex cell sharing the diagonal v0-v7 (corner bits: x, y, z)
 _HEX = ((0, 1, 3, 7), (0, 1, 7, 5), (0, 5, 7, 4), (0, 3, 2, 7), (0, 6, 4, 7), (0, 2, 6, 7))
 

@@ -23,8 +23,8 @@ from .errors import (DanglingVertexError, LevelConstraintError,
                      PlanMeshMismatchError, RestartsExhaustedError,
                      SwapBudgetExceededError, UnrefinableKindError,
                      UnsupportedVersionError, WriteConflictError)
-from .generators import (FAMILIES, GeneratorSpec, gen_quad_rect, gen_tet_prism,
-                         gen_tri_rect, generate, shuffle_elements)
+from .generators import (FAMILIES, GeneratorSpec, gen_hybrid_rect, gen_quad_rect,
+                         gen_tet_prism, gen_tri_rect, generate, shuffle_elements)
 from .mesh import (ConnectivityGraph, Diagnostic, Element, ElementKind, Mesh,
                    Surface, assemble, build_surfaces, connectivity_graph,
                    validate, vizing_bound)

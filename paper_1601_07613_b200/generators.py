@@ -128,6 +128,31 @@ _HEX_SPLIT = np.array([(0, 1, 3, 7), (0, 1, 7, 5), (0, 5, 7, 4),
                       dtype=np.int64)
 
 
+def gen_hybrid_rect(nx: int, ny: int, periodic=False, *, device=None) -> Mesh:
+    """Conforming triangle + quad mix (not a reference generator: the
+    reference's hybrid meshes are its test fixture ``conftest.hybrid_patch``,
+    same layout): cells with i+j even are split along a-c into triangles
+    (a, b, c), (a, c, d), the other cells stay quads (a, b, c, d); elements
+    in cell order.  Colored with the 4-color palette (``coloring.py:38-42``);
+    the DG operator runs it as ``MC_KIND_HYBRID``."""
+    px, py = _pair(periodic)
+    _check_axis("nx", nx, px)
+    _check_axis("ny", ny, py)
+    coords, table = _lattice(nx, ny, px, py)
+    i, j, a, b, c, d = _cell_corners(table, nx, ny)
+    even = (i + j) % 2 == 0
+    # two slots per cell; odd cells use the first only
+    ev = np.full((nx * ny, 2, MAX_ELEM_VERTS), -1, dtype=np.int64)
+    ev[:, 0, 0], ev[:, 0, 1], ev[:, 0, 2] = a, b, c
+    ev[:, 0, 3] = np.where(even, -1, d)
+    ev[:, 1, 0], ev[:, 1, 1], ev[:, 1, 2] = a, c, d
+    kinds = np.empty((nx * ny, 2), np.int8)
+    kinds[:, 0] = np.where(even, KIND_TO_CODE[ElementKind.TRIANGLE], KIND_TO_CODE[ElementKind.QUAD])
+    kinds[:, 1] = KIND_TO_CODE[ElementKind.TRIANGLE]
+    keep = np.stack([np.ones(nx * ny, bool), even], axis=1)
+    return assemble(coords, kinds[keep], ev[keep], device=device)
+
+
 def gen_tet_prism(nx: int, ny: int, nz: int, *, device=None) -> Mesh:
     """Box of unit hex cells, each cut into six positively oriented tets."""
     for name, n in (("nx", nx), ("ny", ny), ("nz", nz)):

@@ -51,22 +51,8 @@ def wave_error(gen, n, p, physics):
 
 
 def gen_hybrid_periodic(n):
-    """Periodic conforming triangle + quad mix (cells with even i+j split
-    into two triangles, the others quads; conftest.hybrid_patch layout)."""
-    from paper_1601_07613_b200.generators import _cell_corners, _lattice
-    from paper_1601_07613_b200.mesh import MAX_ELEM_VERTS
-    coords, table = _lattice(n, n, True, True)
-    i, j, a, b, c, d = _cell_corners(table, n, n)
-    rows, kinds = [], []
-    for k in range(len(a)):
-        if (i[k] + j[k]) % 2 == 0:
-            rows += [(a[k], b[k], c[k], -1), (a[k], c[k], d[k], -1)]
-            kinds += [0, 0]
-        else:
-            rows.append((a[k], b[k], c[k], d[k]))
-            kinds.append(1)
-    ev = np.asarray(rows, dtype=np.int64).reshape(-1, MAX_ELEM_VERTS)
-    return P.assemble(coords, np.asarray(kinds, np.int8), ev)
+    """Periodic conforming triangle + quad mix (``gen_hybrid_rect``)."""
+    return P.gen_hybrid_rect(n, n, (True, True))
 
 
 @pytest.mark.parametrize("gen,physics,p", [

@@ -62,3 +62,14 @@ def test_hybrid_tables(p):
     assert np.array_equal(t.vol_phi[:nq], q.vol_phi)
     assert np.array_equal(t.vol_dphi[:, nq:, :tr.n_basis], tr.vol_dphi)
     assert np.isclose(t.vol_w[:nq].sum(), 1.0) and np.isclose(t.vol_w[nq:].sum(), 0.5)
+
+
+@pytest.mark.parametrize("nx,ny", [(4, 4), (7, 5), (6, 9)])
+def test_gen_hybrid_rect_is_the_reference_fixture_layout(nx, ny):
+    """``gen_hybrid_rect`` builds the reference tests' ``hybrid_patch``
+    (pkg/tests/conftest.py) element for element."""
+    a, b = P.gen_hybrid_rect(nx, ny), hybrid_patch(nx, ny)
+    for f in ("vertices", "elem_kind", "elem_verts", "elem_surfs", "surf_verts", "surf_elems"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    per = P.gen_hybrid_rect(nx, ny, (True, True))
+    assert per.n_elements == a.n_elements and (per.surf_elems[:, 1] >= 0).all()
