@@ -185,6 +185,19 @@ constexpr bool kP1ProjH1 = true;
 constexpr bool kP1ProjH1 = false;
 #endif
 
+// Balanced volume lanes (MC_VOL_BAL; two lanes per side, odd N_eq: lane 0
+// holds NA equations, lane 1 NA + 1): for the volume integral lane 0 also
+// loads the last equation into its spare slot NA, and at each point pair
+// each lane evaluates that equation's trace and projection at its OWN point
+// only (the two partial moments are summed once at the end): 5 instead of
+// 6 trace and projection runs per lane and pair on c4.
+template <class C>
+constexpr bool kVolBal =
+#ifndef MC_VOL_BAL
+    false &&
+#endif
+    Tpe<C>::H == 2 && C::P1PROJ && Tpe<C>::NEQH == Tpe<C>::NA + 1;
+
 // Modes of P_d on the simplex (d < 0: none) and the P_{p-1} modes the
 // reference gradient of mode j needs (modes are ordered by total degree).
 template <int K>
@@ -210,17 +223,36 @@ constexpr int grad_shell(int j) {
 // of point 2i+h only (the traces and the fluxes of the other lane's
 // equations cross by shuffles), so every flux is evaluated once, not twice.
 template <class C, int PH>
-__device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (&u)[Tpe<C>::WH],
+__device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double* svphi,
+                                              const double (&u)[Tpe<C>::WH],
                                               const double* __restrict__ jinv_e, int h,
                                               int nown, bool mine, const Params& P,
-                                              double (&acc)[Tpe<C>::WH]) {
+                                              double (&acc)[Tpe<C>::WH],
+                                              double* jst = nullptr) {
   constexpr int NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH, DIM = C::DIM, M = C::NPL;
   constexpr int H = Tpe<C>::H, WH = Tpe<C>::WH;
   const double* wpsi = vphi + (C::S_WPSI - C::S_VPHI);
   const double* dmat = vphi + (C::S_DMAT - C::S_VPHI);
-  // the Jacobian is needed only at the end: pull its line into L1 now
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(jinv_e));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(jinv_e + DIM * DIM - 1));
+  // the Jacobian is needed only at the end: either copied asynchronously
+  // into the warp scratch now (jst: this side's DIM^2 slot, the side's H
+  // lanes split the copies; cp.async, no registers held) or its line
+  // pulled into L1
+  if (jst) {
+    constexpr int JN = DIM * DIM, PER = (JN + H - 1) / H;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int k = h * PER + i;
+      if (k < JN) {
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(jst + k));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(jinv_e + k)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(jinv_e));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(jinv_e + DIM * DIM - 1));
+  }
   double Pm[DIM][NEQH][M];
 #pragma unroll
   for (int r = 0; r < DIM; ++r)
@@ -248,6 +280,53 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (
   if constexpr (H == 1) {
 #pragma unroll 1
     for (int q = 0; q < C::NQV; ++q) point(q);
+  } else if constexpr (kVolBal<C>) {
+    // slot NA holds the last equation on both lanes; its table rows and
+    // weights are lane-dependent (my point), read from the shared-memory
+    // copy (rows 2i and 2i+1 sit in different banks)
+    constexpr int NA = Tpe<C>::NA;
+    const double* swpsi = svphi + (C::S_WPSI - C::S_VPHI);
+    static_assert(C::NQV % 2 == 0, "balanced volume lanes take point pairs");
+#pragma unroll 1
+    for (int q0 = 0; q0 < C::NQV; q0 += 2) {
+      const int q1 = q0 + 1, qm = q0 + h;
+      double mt[NA], ot[NA];
+#pragma unroll
+      for (int k = 0; k < NA; ++k) {
+        const double a = tdot<NP, WH>(vphi + q0 * C::NPP, u, k * NP);
+        const double b = tdot<NP, WH>(vphi + q1 * C::NPP, u, k * NP);
+        ot[k] = __shfl_xor_sync(kFull, h ? a : b, 1);
+        mt[k] = h ? b : a;
+      }
+      const double last = tdot<NP, WH>(svphi + qm * C::NPP, u, NA * NP);
+      double s[NEQ], F[DIM * NEQ];
+#pragma unroll
+      for (int e = 0; e < NEQ - 1; ++e)
+        s[e] = (e < NA) ? (h == 0 ? mt[e] : ot[e]) : (h == 1 ? mt[e - NA] : ot[e - NA]);
+      s[NEQ - 1] = last;
+      Physics<PH, DIM, NEQ>::pflux(s, P, F);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          const double fm = h ? F[d * NEQ + NA + k] : F[d * NEQ + k];
+          const double fr = __shfl_xor_sync(kFull, h ? F[d * NEQ + k] : F[d * NEQ + NA + k], 1);
+          const double f0 = mine ? (h ? fr : fm) : 0.0;
+          const double f1 = mine ? (h ? fm : fr) : 0.0;
+#pragma unroll
+          for (int m = 0; m < M; ++m)
+            Pm[d][k][m] = fma(wpsi[q1 * M + m], f1, fma(wpsi[q0 * M + m], f0, Pm[d][k][m]));
+        }
+        const double fl = mine ? F[d * NEQ + NEQ - 1] : 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) Pm[d][NA][m] = fma(swpsi[qm * M + m], fl, Pm[d][NA][m]);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        Pm[d][NA][m] += __shfl_xor_sync(kFull, Pm[d][NA][m], 1);
   } else {
     constexpr int NA = Tpe<C>::NA;
 #ifndef MC_PAIR_UNROLL
@@ -317,8 +396,15 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double (
   }
   // physical -> contravariant moments with the element's inverse Jacobian
   double ji[DIM * DIM];
+  if (jst) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
 #pragma unroll
-  for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
+    for (int k = 0; k < DIM * DIM; ++k) ji[k] = jst[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
+  }
 #pragma unroll
   for (int k = 0; k < NEQH; ++k)
 #pragma unroll
@@ -353,7 +439,8 @@ template <class C, int PH>
 __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[Tpe<C>::WH],
                                            const double* __restrict__ jinv_e, int h, int nown,
                                            bool mine, const Params& P,
-                                           double (&acc)[Tpe<C>::WH], int ek = 0) {
+                                           double (&acc)[Tpe<C>::WH], int ek = 0,
+                                           double* jst = nullptr) {
   constexpr int WH = Tpe<C>::WH, NP = C::NP, NEQ = C::NEQ, NEQH = Tpe<C>::NEQH, DIM = C::DIM;
   const double* vphi = vol_tables<C, true>(st);
   const double* vdphi = vphi + (C::S_VDPHI - C::S_VPHI);
@@ -361,7 +448,7 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   // two lanes per side (tets): c4 first-touch color 4.91 -> 4.57 ms; one
   // lane (c2 triangles) measured slower (color 1 3.55 -> 3.27 TB/s)
   if constexpr (C::P1PROJ && (Tpe<C>::H == 2 || kP1ProjH1)) {
-    tpe_volume_p1<C, PH>(vphi, u, jinv_e, h, nown, mine, P, acc);
+    tpe_volume_p1<C, PH>(vphi, st + C::S_VPHI, u, jinv_e, h, nown, mine, P, acc, jst);
     return;
   }
   double ji[DIM * DIM];
@@ -496,6 +583,12 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   }
 }
 
+
+// lane 0's spare equation slot NA of its coefficient array (kVolBal)
+template <class C>
+__device__ __forceinline__ double (&bal_slot(double (&u)[Tpe<C>::WH]))[C::NP] {
+  return *reinterpret_cast<double(*)[C::NP]>(&u[Tpe<C>::NA * C::NP]);
+}
 
 struct TpeSide {
   int e, mycode;
@@ -1127,7 +1220,10 @@ __device__ __forceinline__ void tpe_stage(const double* __restrict__ g, double* 
 #define MC_TPE_MINB_VOL 0   // 0: Tpe<C>::MINB
 #endif
 #ifndef MC_TPE_MINB_VOL2
-#define MC_TPE_MINB_VOL2 3  // two lanes per side, first-touch passes (tets)
+// two lanes per side, first-touch passes (tets): 2 blocks per SM (255
+// registers, no spills) since the face-table-row change; 3 blocks (168
+// registers, 104-byte spills) measured 1.414 vs 1.447 G edges/s on c4
+#define MC_TPE_MINB_VOL2 2
 #endif
 
 // surface-flux scheme per kernel variant: warp flux tasks (Tpe::TASKS /
@@ -1235,6 +1331,11 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
     }
+    if constexpr (kVol && kVolBal<C>) {   // lane 0: the last equation in its spare slot
+      if (ln.h == 0 && first)
+        sload<C::NP, true, false>(U + int64_t(t.e) * v.stride + (C::NEQ - 1) * C::NP, C::NP,
+                                  bal_slot<C>(u));
+    }
     // first-touch passes: the volume integral first, then the residual
     // blocks of the sides touched before (acc is not live during the volume)
     if (kVol || !(t.owner && !first)) {
@@ -1250,7 +1351,14 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
       if constexpr (T::H == 1) {
         if (first) tpe_volume<C, PH>(st, u, jp, 0, ln.nown, true, v.prm, acc, ek);
       } else if (__any_sync(kFull, first)) {   // the whole warp takes part in the shuffles
-        tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc, ek);
+#ifdef MC_JINV_ASYNC
+        // the Jacobian through the (idle) flux-task scratch, one slot per side
+        double* jst = kVariantTasks<T, kRK, kVol>
+                          ? ws + (ln.lane / T::H) * (C::DIM * C::DIM) : nullptr;
+#else
+        double* jst = nullptr;
+#endif
+        tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc, ek, jst);
       }
       if (t.owner && !first) sload_rw<WH, kWhole, T::V4>(R + off, n, acc);
     }
@@ -1359,6 +1467,10 @@ k_tpe_volume(View v, const double* __restrict__ U, double* __restrict__ R) {
     else {
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
+    }
+    if constexpr (kVolBal<C>) {
+      if (h == 0 && has)
+        tload<C::NP, true, false>(U + e * v.stride + (C::NEQ - 1) * C::NP, C::NP, bal_slot<C>(u));
     }
 #pragma unroll
     for (int j = 0; j < WH; ++j) acc[j] = 0.0;
