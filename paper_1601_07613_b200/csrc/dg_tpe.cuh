@@ -378,7 +378,9 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double* 
         for (int k = 0; k < NEQH; ++k) {
           const double fm = own_part<C>(F + d * NEQ, h, k);
           const double fr = __shfl_xor_sync(kFull, own_part<C>(F + d * NEQ, h ^ 1, k), 1);
-#ifdef MC_PAIR_NO_ON   // no zeroing: garbage stays in non-contributing lane pairs
+#ifndef MC_PAIR_ZERO_IDLE   // no zeroing (c4 color 1 +1.6 %): garbage stays in
+                            // non-contributing lane pairs, whose acc is replaced
+                            // (residual load) or never stored
           const double f0 = h ? fr : fm;
           const double f1 = h ? fm : fr;
 #else
@@ -1351,8 +1353,9 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
       if constexpr (T::H == 1) {
         if (first) tpe_volume<C, PH>(st, u, jp, 0, ln.nown, true, v.prm, acc, ek);
       } else if (__any_sync(kFull, first)) {   // the whole warp takes part in the shuffles
-#ifdef MC_JINV_ASYNC
+#ifndef MC_NO_JINV_ASYNC
         // the Jacobian through the (idle) flux-task scratch, one slot per side
+        // (c4 color 1 +2 % at 2 blocks/SM: the lift no longer waits on its loads)
         double* jst = kVariantTasks<T, kRK, kVol>
                           ? ws + (ln.lane / T::H) * (C::DIM * C::DIM) : nullptr;
 #else
