@@ -31,7 +31,8 @@ cpu_baseline / --impl reference = the numpy fp64 DG oracle (a port: the
             oracle/ only and never loads the product library.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                       [--config c1|c2|c3|c4|c5] [--no-variants] [--no-cpu]
+                       [--config c1|c2|c3|c4|c5|h1] [--no-variants] [--no-cpu]
+                       [--exchange nccl|push] [--state f64|f32]
        python bench.py --layouts     # the paper's Table 7 layouts on c2
 """
 
@@ -648,7 +649,8 @@ def variants(op, U_host, stream, reps=5):
     out["colored_vs_buffered"] = out["rhs_buffered_ms"] / out["rhs_colored_ms"]
     out["colored_vs_atomic"] = out["rhs_atomic_ms"] / out["rhs_colored_ms"]
     mem = P.memory_saved(op.degree, op.n_equations, op.n_surfaces,
-                         {"tri": "tri", "quad": "quad", "tet": "tet"}[op.kind.value])
+                         {"tri": "tri", "quad": "quad", "tet": "tet",
+                          "hybrid": "quad"}[op.kind.value])   # hybrid slots are quad-sized
     out["buffer_bytes_avoided"] = mem.n_bytes
     out["buffer_gb_truncated"] = mem.gb_truncated
     del R
