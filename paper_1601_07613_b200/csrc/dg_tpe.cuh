@@ -90,7 +90,10 @@ struct Tpe {
 #ifdef MC_NO_SURF_TASKS
   static constexpr bool TASKS_SURF = TASKS;
 #else
-  static constexpr bool TASKS_SURF = TASKS || H == 2;
+  // only when the (surface, point) tasks fill the warp: 3-point edges (p =
+  // 2 quads, hybrid meshes) leave a quarter of the lanes idle and measured
+  // slower (h1 1.29 -> 1.35 G edges/s with per-lane fluxes)
+  static constexpr bool TASKS_SURF = TASKS || (H == 2 && (16 / (H ? H : 1)) * C::NQF >= 32);
 #endif
   static constexpr int SMEM = (C::S_TOTAL + (TASKS ? 4 * X_SIZE : 0)) * 8;
   static constexpr int SMEM_SURF = (C::S_TOTAL + (TASKS_SURF ? 4 * X_SIZE : 0)) * 8;
@@ -456,17 +459,18 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
   double ji[DIM * DIM];
 #pragma unroll
   for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
-#ifndef MC_NO_QUAD_SF
-  if constexpr (C::KIND == QUAD && Tpe<C>::H == 2) {
-    // tensor-product quads: sum factorisation (basis l_i(x) l_j(y), Gauss
-    // points (x_a, y_b)), half the multiply-adds of the dense contraction.
-    //   trace:      T[j] = sum_i l_i(x_a) u[i][j];  U(a,b) = sum_j l_j(y_b) T[j]
-    //   projection: A[j] += w_ab l_j(y_b) F0, B[j] += w_ab l'_j(y_b) F1 over b,
-    //               then acc[i][j] += l'_i(x_a) A[j] + l_i(x_a) B[j]
-    // The 1D values are entries of the 2D tables (l_0 = 1 for the
-    // orthonormal basis on [0,1]).
+  // tensor-product quads (QUAD, and the quads of a HYB mesh): sum
+  // factorisation (basis l_i(x) l_j(y), Gauss points (x_a, y_b)), half the
+  // multiply-adds of the dense contraction.
+  //   trace:      T[j] = sum_i l_i(x_a) u[i][j];  U(a,b) = sum_j l_j(y_b) T[j]
+  //   projection: A[j] += w_ab l_j(y_b) F0, B[j] += w_ab l'_j(y_b) F1 over b,
+  //               then acc[i][j] += l'_i(x_a) A[j] + l_i(x_a) B[j]
+  // The 1D values are entries of the 2D tables (l_0 = 1 for the
+  // orthonormal basis on [0,1]); `onk` = this lane's element is a quad.
+  auto quad_sf = [&](bool onk) {
+    if constexpr (C::KIND == QUAD || C::KIND == HYB) {
     constexpr int n = C::PDEG + 1;
-    static_assert(n * n == NP && n * n == C::NQV, "tensor quad layout");
+    static_assert(n * n == NP && n * n == C::NQV_QUAD, "tensor quad layout");
     auto L1 = [&](int a, int i) { return vphi[(a * n) * C::NPP + i * n]; };
     auto D1 = [&](int a, int i) { return vdphi[(a * n) * C::NPP + i * n]; };
 #pragma unroll 1
@@ -498,7 +502,7 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
         const double w = vw[a * n + b];
 #pragma unroll
         for (int k = 0; k < NEQH; ++k) {
-          const bool on = mine && k < nown;
+          const bool on = mine && onk && k < nown;
           const double g0 = on ? w * own_part<C>(Ft, h, k) : 0.0;
           const double g1 = on ? w * own_part<C>(Ft + NEQ, h, k) : 0.0;
 #pragma unroll
@@ -517,6 +521,11 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
             acc[k * NP + i * n + j] =
                 fma(D1(a, i), A[k][j], fma(L1(a, i), B[k][j], acc[k * NP + i * n + j]));
     }
+    }
+  };
+#ifndef MC_NO_QUAD_SF
+  if constexpr (C::KIND == QUAD && Tpe<C>::H == 2) {
+    quad_sf(true);
     return;
   }
 #endif
@@ -577,7 +586,13 @@ __device__ __forceinline__ void tpe_volume(const double* st, const double (&u)[T
       if (ek) points(0, C::NQV_QUAD, true);
       else points(C::NQV_QUAD, C::NQV, true);
     } else {                          // the whole warp takes part (shuffles)
-      if (__any_sync(kFull, mine && ek)) points(0, C::NQV_QUAD, ek != 0);
+      if (__any_sync(kFull, mine && ek)) {
+#ifndef MC_NO_QUAD_SF
+        quad_sf(ek != 0);
+#else
+        points(0, C::NQV_QUAD, ek != 0);
+#endif
+      }
       if (__any_sync(kFull, mine && !ek)) points(C::NQV_QUAD, C::NQV, ek == 0);
     }
   } else {
