@@ -110,3 +110,15 @@ def test_hybrid_fp32_state_within_1e5(cuda):
     U = op.initial_state("wave")
     dt = op.stable_dt(0.2)
     assert rel(op.ssprk3(U, dt, 2), D.ssprk3(prob, U, dt, 2)) < 1e-5
+
+
+@pytest.mark.parametrize("ordering", ["sfc", "reorder", "renumber", "none"])
+def test_hybrid_layouts(cuda, ordering):
+    """Every element / surface layout of the operator on a hybrid mesh."""
+    mesh = P.shuffle_elements(P.gen_hybrid_rect(9, 7), 2)
+    op = DGOperator(mesh, P.color(mesh)[0], degree=2, physics="euler", ordering=ordering)
+    prob = D.problem_from(op.oracle_problem())
+    U = op.initial_state("wave")
+    assert D.rel_error(op.rhs(U), D.rhs(prob, U), prob, U) < TOL
+    dt = op.stable_dt(0.2)
+    assert rel(op.ssprk3(U, dt, 2), D.ssprk3(prob, U, dt, 2)) < TOL
