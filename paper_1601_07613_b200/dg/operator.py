@@ -36,10 +36,12 @@ from .layout import (build_surface_list, element_centroids, element_kinds, mesh_
 
 _KIND_CODE = {ElementKind.TRIANGLE: 0, ElementKind.QUAD: 1, ElementKind.TET: 2, HYBRID: 3}
 _STRATEGY = {"colored": 0, "buffered": 1, "atomic": 2}
-# tets: sort colors >= 2 by side codes inside windows of 4096 surfaces (warps
-# read the same face-table rows; the element order survives at a coarse
-# scale): c4 1.223 -> 1.239 G edges/s, surface-only colors +3.7 %
-_TET_CODE_SORT = 4096
+# tets: unsorted.  The windowed side-code sort (colors >= 2 sorted inside
+# windows of 4096 surfaces so warps read the same face-table rows) paid in
+# round 1 (c4 1.223 -> 1.239 G edges/s); since the face-table row is read
+# once per point it costs more coalescing than it saves (c4 1.454 -> 1.487
+# unsorted).  MC_CODE_SORT=4096 restores it.
+_TET_CODE_SORT = False
 
 
 def _sort_options(code_sort, kind) -> dict:
@@ -49,8 +51,8 @@ def _sort_options(code_sort, kind) -> dict:
     the same face-table rows); an int n >= 2 = sort colors >= 2 inside
     windows of n surfaces counted from the color's first surface (color 1
     stays coalesced).  None = the measured default per element kind
-    (whole-color sort +2 % on quads, windows of 4096 on tets,
-    unsorted on triangles), overridable with MC_CODE_SORT."""
+    (whole-color sort +2 % on quads, unsorted on tets and
+    triangles), overridable with MC_CODE_SORT."""
     if code_sort is None:
         env = os.environ.get("MC_CODE_SORT")
         if env is not None:
