@@ -973,33 +973,58 @@ __device__ __forceinline__ void tpe_surface(const double* st, const TpeSide& t, 
 // L1 allocation (L1::no_allocate): c3 1.30 -> 1.43 G edges/s, surface-only
 // colors 4.5 -> 5.1-5.3 TB/s; c2 neutral to +1 %.  MC_L1_ALLOC restores the
 // default caching.
-#ifdef MC_L1_ALLOC
-#define MC_LD_NC "ld.global.nc.v4.f64"
-#define MC_LD_RW "ld.global.v4.f64"
-#define MC_LD2_NC "ld.global.nc.v2.f64"
-#define MC_LD2_RW "ld.global.v2.f64"
+// Tets (c4) measured the other way round once the face-table row was read
+// once per point and the colors stopped being side-code sorted: default L1
+// allocation 1.483 -> 1.504 G edges/s (colors 2-4 +1.5-3 %), so the policy
+// is a template parameter: kL1 = true allocates in L1 (kTpeL1<C>).
+// MC_L1_ALLOC / MC_L1_NOALLOC force one policy everywhere.
+#define MC_LD_NC_A "ld.global.nc.v4.f64"
+#define MC_LD_RW_A "ld.global.v4.f64"
+#define MC_LD2_NC_A "ld.global.nc.v2.f64"
+#define MC_LD2_RW_A "ld.global.v2.f64"
+#define MC_LD_NC_N "ld.global.nc.L1::no_allocate.v4.f64"
+#define MC_LD_RW_N "ld.global.L1::no_allocate.v4.f64"
+#define MC_LD2_NC_N "ld.global.nc.L1::no_allocate.v2.f64"
+#define MC_LD2_RW_N "ld.global.L1::no_allocate.v2.f64"
+template <class C>
+constexpr bool kTpeL1 =
+#if defined(MC_L1_ALLOC)
+    true;
+#elif defined(MC_L1_NOALLOC)
+    false;
 #else
-#define MC_LD_NC "ld.global.nc.L1::no_allocate.v4.f64"
-#define MC_LD_RW "ld.global.L1::no_allocate.v4.f64"
-#define MC_LD2_NC "ld.global.nc.L1::no_allocate.v2.f64"
-#define MC_LD2_RW "ld.global.L1::no_allocate.v2.f64"
+    C::DIM == 3;
 #endif
+template <bool kL1 = false>
 __device__ __forceinline__ void ld4_nc(const double* p, double& a, double& b, double& c, double& d) {
-  asm(MC_LD_NC " {%0,%1,%2,%3}, [%4];"
-      : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+  if constexpr (kL1)
+    asm(MC_LD_NC_A " {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+  else
+    asm(MC_LD_NC_N " {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
+template <bool kL1 = false>
 __device__ __forceinline__ void ld4(const double* p, double& a, double& b, double& c, double& d) {
-  asm(MC_LD_RW " {%0,%1,%2,%3}, [%4];"
-      : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+  if constexpr (kL1)
+    asm(MC_LD_RW_A " {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+  else
+    asm(MC_LD_RW_N " {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
+template <bool kL1 = false>
 __device__ __forceinline__ double2 ld2_nc(const double* p) {
   double2 r;
-  asm(MC_LD2_NC " {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  if constexpr (kL1)
+    asm(MC_LD2_NC_A " {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  else
+    asm(MC_LD2_NC_N " {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
+template <bool kL1 = false>
 __device__ __forceinline__ double2 ld2(const double* p) {
   double2 r;
-  asm(MC_LD2_RW " {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  if constexpr (kL1)
+    asm(MC_LD2_RW_A " {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  else
+    asm(MC_LD2_RW_N " {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
 __device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
@@ -1009,19 +1034,19 @@ __device__ __forceinline__ void st4(double* p, double a, double b, double c, dou
 
 // This lane's run of `n` doubles (n <= N): the whole block when H = 1
 // (256-bit when N % 4 == 0), its equation group when H = 2 (128-bit pairs).
-template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0)>
+template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0), bool kL1 = false>
 __device__ __forceinline__ void tload(const double* __restrict__ src, int n, double (&dst)[N]) {
   if constexpr (kV4) {   // 32-byte chunks, a 16-byte tail when N % 4 == 2
 #pragma unroll
     for (int j = 0; j < N / 4; ++j) {
       if (kWhole || 4 * j + 4 <= n)
-        ld4_nc(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
+        ld4_nc<kL1>(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
       else
         dst[4 * j] = dst[4 * j + 1] = dst[4 * j + 2] = dst[4 * j + 3] = 0.0;
     }
     if constexpr (N % 4 == 2) {
       if (kWhole || N <= n) {
-        const double2 a = ld2_nc(src + N - 2);
+        const double2 a = ld2_nc<kL1>(src + N - 2);
         dst[N - 2] = a.x;
         dst[N - 1] = a.y;
       } else {
@@ -1032,7 +1057,7 @@ __device__ __forceinline__ void tload(const double* __restrict__ src, int n, dou
 #pragma unroll
     for (int j = 0; j < N / 2; ++j) {
       if (kWhole || 2 * j < n) {
-        const double2 a = ld2_nc(src + 2 * j);
+        const double2 a = ld2_nc<kL1>(src + 2 * j);
         dst[2 * j] = a.x;
         dst[2 * j + 1] = a.y;
       } else {
@@ -1045,19 +1070,19 @@ __device__ __forceinline__ void tload(const double* __restrict__ src, int n, dou
   }
 }
 
-template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0)>
+template <int N, bool kWhole, bool kV4 = kWhole && (N % 4 == 0), bool kL1 = false>
 __device__ __forceinline__ void tload_rw(const double* src, int n, double (&dst)[N]) {
   if constexpr (kV4) {
 #pragma unroll
     for (int j = 0; j < N / 4; ++j) {
       if (kWhole || 4 * j + 4 <= n)
-        ld4(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
+        ld4<kL1>(src + 4 * j, dst[4 * j], dst[4 * j + 1], dst[4 * j + 2], dst[4 * j + 3]);
       else
         dst[4 * j] = dst[4 * j + 1] = dst[4 * j + 2] = dst[4 * j + 3] = 0.0;
     }
     if constexpr (N % 4 == 2) {
       if (kWhole || N <= n) {
-        const double2 a = ld2(src + N - 2);
+        const double2 a = ld2<kL1>(src + N - 2);
         dst[N - 2] = a.x;
         dst[N - 1] = a.y;
       } else {
@@ -1068,7 +1093,7 @@ __device__ __forceinline__ void tload_rw(const double* src, int n, double (&dst)
 #pragma unroll
     for (int j = 0; j < N / 2; ++j) {
       if (kWhole || 2 * j < n) {
-        const double2 a = ld2(src + 2 * j);
+        const double2 a = ld2<kL1>(src + 2 * j);
         dst[2 * j] = a.x;
         dst[2 * j + 1] = a.y;
       } else {
@@ -1184,20 +1209,20 @@ __device__ __forceinline__ void fstore2(float* dst, int n, const double (&src)[N
 }
 
 // state-type dispatch: S = double (the default) or float
-template <int N, bool kWhole, bool kV4>
+template <int N, bool kWhole, bool kV4, bool kL1 = false>
 __device__ __forceinline__ void sload(const double* src, int n, double (&dst)[N]) {
-  tload<N, kWhole, kV4>(src, n, dst);
+  tload<N, kWhole, kV4, kL1>(src, n, dst);
 }
-template <int N, bool kWhole, bool kV4>
+template <int N, bool kWhole, bool kV4, bool kL1 = false>
 __device__ __forceinline__ void sload(const float* src, int n, double (&dst)[N]) {
   if constexpr (kWhole || kV4) fload<N, kWhole>(src, n, dst, true);
   else fload2<N, kWhole>(src, n, dst, true);
 }
-template <int N, bool kWhole, bool kV4>
+template <int N, bool kWhole, bool kV4, bool kL1 = false>
 __device__ __forceinline__ void sload_rw(const double* src, int n, double (&dst)[N]) {
-  tload_rw<N, kWhole, kV4>(src, n, dst);
+  tload_rw<N, kWhole, kV4, kL1>(src, n, dst);
 }
-template <int N, bool kWhole, bool kV4>
+template <int N, bool kWhole, bool kV4, bool kL1 = false>
 __device__ __forceinline__ void sload_rw(const float* src, int n, double (&dst)[N]) {
   if constexpr (kWhole || kV4) fload<N, kWhole>(src, n, dst, false);
   else fload2<N, kWhole>(src, n, dst, false);
@@ -1343,7 +1368,7 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
     }
 #endif
     double u[WH], acc[WH];
-    if (t.has) sload<WH, kWhole, T::V4>(U + off, n, u);
+    if (t.has) sload<WH, kWhole, T::V4, kTpeL1<C>>(U + off, n, u);
     else {
 #pragma unroll
       for (int j = 0; j < WH; ++j) u[j] = 0.0;
@@ -1359,7 +1384,7 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
 #pragma unroll
       for (int j = 0; j < WH; ++j) acc[j] = 0.0;
     } else {
-      sload_rw<WH, kWhole, T::V4>(R + off, n, acc);
+      sload_rw<WH, kWhole, T::V4, kTpeL1<C>>(R + off, n, acc);
     }
     if constexpr (kVol) {
       const double* jp = v.jinv + int64_t(first ? t.e : 0) * (C::DIM * C::DIM);
@@ -1378,7 +1403,7 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
 #endif
         tpe_volume<C, PH>(st, u, jp, ln.h, ln.nown, first, v.prm, acc, ek, jst);
       }
-      if (t.owner && !first) sload_rw<WH, kWhole, T::V4>(R + off, n, acc);
+      if (t.owner && !first) sload_rw<WH, kWhole, T::V4, kTpeL1<C>>(R + off, n, acc);
     }
     tpe_surface<C, PH, kVariantTasks<T, kRK, kVol>>(st, t, ln.side, ln.h, ln.nown, u, v.prm, acc,
                                                      ln.grp, ws);
@@ -1387,12 +1412,12 @@ k_tpe_colored(View v, S* __restrict__ U, S* __restrict__ R, RK rk, int64_t begin
 #ifdef MC_RK_RELOAD_U
         // re-read the element's own block (L2) instead of keeping u live
         // through the surface work (fewer registers in the last-touch pass)
-        if constexpr (kRK && !kVol) sload<WH, kWhole, T::V4>(U + off, n, u);
+        if constexpr (kRK && !kVol) sload<WH, kWhole, T::V4, kTpeL1<C>>(U + off, n, u);
 #endif
         if (rk.save_u0) sstore<WH, kWhole, T::V4>(U0 + off, n, u);
         if (rk.a != 0.0) {
           double u0[WH];
-          sload<WH, kWhole, T::V4>(U0 + off, n, u0);
+          sload<WH, kWhole, T::V4, kTpeL1<C>>(U0 + off, n, u0);
 #pragma unroll
           for (int j = 0; j < WH; ++j) acc[j] = rk.a * u0[j] + rk.b * fma(rk.dt, acc[j], u[j]);
         } else {
