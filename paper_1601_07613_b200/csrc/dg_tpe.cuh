@@ -201,6 +201,19 @@ constexpr bool kVolBal =
 #endif
     Tpe<C>::H == 2 && C::P1PROJ && Tpe<C>::NEQH == Tpe<C>::NA + 1;
 
+// Mode-split projection (two lanes per side, even NPL): at each point pair
+// both lanes hold the full flux of their own point; lane h accumulates the
+// P_{p-1} modes [h*NPL/2, (h+1)*NPL/2) of ALL equations at both points (the
+// partner's fluxes cross by one shuffle each), so the projection needs no
+// per-component selects and no dead spare-slot equation; the two mode halves
+// of each lane's own equations cross once per element before the lift.
+template <class C>
+constexpr bool kVolMsplit =
+#ifdef MC_VOL_NO_MSPLIT
+    false &&
+#endif
+    Tpe<C>::H == 2 && C::P1PROJ && C::NPL % 2 == 0 && !kVolBal<C>;
+
 // Modes of P_d on the simplex (d < 0: none) and the P_{p-1} modes the
 // reference gradient of mode j needs (modes are ordered by total degree).
 template <int K>
@@ -280,9 +293,114 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double* 
         for (int m = 0; m < M; ++m) Pm[d][k][m] = fma(wpsi[q * M + m], f, Pm[d][k][m]);
       }
   };
+  auto load_ji = [&](double (&ji)[DIM * DIM]) {
+    if (jst) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < DIM * DIM; ++k) ji[k] = jst[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
+    }
+  };
   if constexpr (H == 1) {
 #pragma unroll 1
     for (int q = 0; q < C::NQV; ++q) point(q);
+  } else if constexpr (kVolMsplit<C>) {
+    constexpr int NA = Tpe<C>::NA, MH = M / 2;
+    // this lane's modes of the weighted P_{p-1} table (shared-memory copy:
+    // the row depends on the lane)
+    const double* wmine = svphi + (C::S_WPSI - C::S_VPHI) + h * MH;
+    double Q[DIM][NEQ][MH];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+#pragma unroll
+      for (int k = 0; k < NEQ; ++k)
+#pragma unroll
+        for (int m = 0; m < MH; ++m) Q[d][k][m] = 0.0;
+#pragma unroll 1
+    for (int q0 = 0; q0 + 1 < C::NQV; q0 += 2) {
+      const int q1 = q0 + 1;
+      double mt[NEQH], ot[NEQH];
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k) {
+        const double a = tdot<NP, WH>(vphi + q0 * C::NPP, u, k * NP);
+        const double b = tdot<NP, WH>(vphi + q1 * C::NPP, u, k * NP);
+        ot[k] = __shfl_xor_sync(kFull, h ? a : b, 1);
+        mt[k] = h ? b : a;
+      }
+      double s[NEQ], F[DIM * NEQ];
+#pragma unroll
+      for (int e = 0; e < NEQ; ++e)
+        s[e] = (e < NA) ? (h == 0 ? mt[e] : ot[e]) : (h == 1 ? mt[e - NA] : ot[e - NA]);
+      Physics<PH, DIM, NEQ>::pflux(s, P, F);
+      const int qm = q0 + h, qo = q1 - h;
+      double wm[MH], wo[MH];
+#pragma unroll
+      for (int m = 0; m < MH; ++m) {
+        wm[m] = wmine[qm * M + m];
+        wo[m] = wmine[qo * M + m];
+      }
+      // idle lane pairs accumulate garbage that never leaves the pair (as
+      // in the equation-split loop below)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d)
+#pragma unroll
+        for (int k = 0; k < NEQ; ++k) {
+          const double fm = F[d * NEQ + k];
+          const double fo = __shfl_xor_sync(kFull, fm, 1);
+#pragma unroll
+          for (int m = 0; m < MH; ++m) Q[d][k][m] = fma(wo[m], fo, fma(wm[m], fm, Q[d][k][m]));
+        }
+    }
+    if constexpr (C::NQV % 2) {   // last point: both lanes evaluate it
+      constexpr int q = C::NQV - 1;
+      double own[NEQH], s[NEQ], F[DIM * NEQ];
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k) own[k] = tdot<NP, WH>(vphi + q * C::NPP, u, k * NP);
+      assemble_state<C>(own, h, s);
+      Physics<PH, DIM, NEQ>::pflux(s, P, F);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d)
+#pragma unroll
+        for (int k = 0; k < NEQ; ++k)
+#pragma unroll
+          for (int m = 0; m < MH; ++m) Q[d][k][m] = fma(wmine[q * M + m], F[d * NEQ + k], Q[d][k][m]);
+    }
+    double ji[DIM * DIM];
+    load_ji(ji);
+#pragma unroll
+    for (int k = 0; k < NEQ; ++k)
+#pragma unroll
+      for (int m = 0; m < MH; ++m) {
+        double pd[DIM];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) pd[d] = Q[d][k][m];
+#pragma unroll
+        for (int r = 0; r < DIM; ++r) {
+          double t = 0.0;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) t = fma(ji[r * DIM + d], pd[d], t);
+          Q[r][k][m] = t;
+        }
+      }
+    // my equations' contravariant moments: my mode half, the partner's by
+    // shuffle (lane 0 holds modes [0, MH), lane 1 [MH, M))
+#pragma unroll
+    for (int r = 0; r < DIM; ++r)
+#pragma unroll
+      for (int k = 0; k < NEQH; ++k) {
+        const int k1 = (NA + k < NEQ) ? NA + k : NEQ - 1;   // lane 1's slot-k equation
+#pragma unroll
+        for (int m = 0; m < MH; ++m) {
+          const double q0v = Q[r][k][m], q1v = Q[r][k1][m];
+          const double mine_v = h ? q1v : q0v;
+          const double recv = __shfl_xor_sync(kFull, h ? q0v : q1v, 1);
+          Pm[r][k][m] = h ? recv : mine_v;
+          Pm[r][k][MH + m] = h ? mine_v : recv;
+        }
+      }
   } else if constexpr (kVolBal<C>) {
     // slot NA holds the last equation on both lanes; its table rows and
     // weights are lane-dependent (my point), read from the shared-memory
@@ -400,16 +518,10 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double* 
     if constexpr (C::NQV % 2) point(C::NQV - 1);
   }
   // physical -> contravariant moments with the element's inverse Jacobian
+  // (the mode-split branch has done it on its own layout)
+  if constexpr (!kVolMsplit<C>) {
   double ji[DIM * DIM];
-  if (jst) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < DIM * DIM; ++k) ji[k] = jst[k];
-  } else {
-#pragma unroll
-    for (int k = 0; k < DIM * DIM; ++k) ji[k] = __ldg(jinv_e + k);
-  }
+  load_ji(ji);
 #pragma unroll
   for (int k = 0; k < NEQH; ++k)
 #pragma unroll
@@ -425,6 +537,7 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double* 
         Pm[r][k][m] = t;
       }
     }
+  }
 #pragma unroll
   for (int k = 0; k < NEQH; ++k)
 #pragma unroll
