@@ -212,7 +212,7 @@ constexpr bool kVolMsplit =
 #ifdef MC_VOL_NO_MSPLIT
     false &&
 #endif
-    Tpe<C>::H == 2 && C::P1PROJ && C::NPL % 2 == 0 && !kVolBal<C>;
+    Tpe<C>::H == 2 && C::P1PROJ && C::NPL % 2 == 0;
 
 // Modes of P_d on the simplex (d < 0: none) and the P_{p-1} modes the
 // reference gradient of mode j needs (modes are ordered by total degree).
@@ -322,20 +322,32 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double* 
 #pragma unroll 1
     for (int q0 = 0; q0 + 1 < C::NQV; q0 += 2) {
       const int q1 = q0 + 1;
+      const int qm = q0 + h, qo = q1 - h;
+      // balanced lanes (kVolBal): the shared equations at both points, the
+      // last one (both lanes hold it in slot NA) at this lane's point only
+      constexpr int NT = kVolBal<C> ? NA : NEQH;
       double mt[NEQH], ot[NEQH];
+#ifdef MC_VOL_TRACE_SMEM   // lane-dependent rows from the shared copy: no selects
 #pragma unroll
-      for (int k = 0; k < NEQH; ++k) {
+      for (int k = 0; k < NT; ++k) {
+        ot[k] = __shfl_xor_sync(kFull, tdot<NP, WH>(svphi + qo * C::NPP, u, k * NP), 1);
+        mt[k] = tdot<NP, WH>(svphi + qm * C::NPP, u, k * NP);
+      }
+#else
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
         const double a = tdot<NP, WH>(vphi + q0 * C::NPP, u, k * NP);
         const double b = tdot<NP, WH>(vphi + q1 * C::NPP, u, k * NP);
         ot[k] = __shfl_xor_sync(kFull, h ? a : b, 1);
         mt[k] = h ? b : a;
       }
+#endif
       double s[NEQ], F[DIM * NEQ];
 #pragma unroll
       for (int e = 0; e < NEQ; ++e)
         s[e] = (e < NA) ? (h == 0 ? mt[e] : ot[e]) : (h == 1 ? mt[e - NA] : ot[e - NA]);
+      if constexpr (kVolBal<C>) s[NEQ - 1] = tdot<NP, WH>(svphi + qm * C::NPP, u, NA * NP);
       Physics<PH, DIM, NEQ>::pflux(s, P, F);
-      const int qm = q0 + h, qo = q1 - h;
       double wm[MH], wo[MH];
 #pragma unroll
       for (int m = 0; m < MH; ++m) {
