@@ -319,7 +319,11 @@ __device__ __forceinline__ void tpe_volume_p1(const double* vphi, const double* 
       for (int k = 0; k < NEQ; ++k)
 #pragma unroll
         for (int m = 0; m < MH; ++m) Q[d][k][m] = 0.0;
-#pragma unroll 1
+#ifndef MC_MSPLIT_UNROLL
+#define MC_MSPLIT_UNROLL 1
+#endif
+    constexpr int kMsUnroll = MC_MSPLIT_UNROLL;
+#pragma unroll kMsUnroll
     for (int q0 = 0; q0 + 1 < C::NQV; q0 += 2) {
       const int q1 = q0 + 1;
       const int qm = q0 + h, qo = q1 - h;
